@@ -1,0 +1,160 @@
+/*
+ * pms.h -- C ABI of the B200 (sm_100a) Skip-Brute-Force planted (l,d) motif
+ * search library, libpms_b200.so.
+ *
+ * Operation (section I.A problem statement; PAPER.md:63 section
+ * III.A skip-brute-force; section IV.A candidates generated from
+ * their index): given n DNA sequences s_0..s_{n-1} of length t over
+ * {A,C,G,T}, return every l-mer m such that EVERY sequence has a window
+ * (length-l substring, t-l+1 of them) at Hamming distance <= d from m.
+ * The search enumerates all 4^l candidates and abandons a candidate at the
+ * first sequence with no such window (the skip rule).  The result is a
+ * set; it does not depend on the skip rule, the scan order or the launch
+ * configuration.
+ *
+ * Codes: A=0 C=1 G=2 T=3; an l-mer's code is big-endian base 4 (first base in
+ * the most significant digit), so code order = lexicographic order (SPEC.md:
+ * 66-74).  l <= 16, so a code fits uint32.
+ *
+ * Conventions for every entry point:
+ *   - sizes are element counts unless stated; all functions are thread-safe
+ *     for distinct plans; a plan is used by one host thread at a time;
+ *   - the caller owns every buffer it passes; the library keeps no pointer
+ *     to caller memory after a call returns (pms_plan_execute: until the work
+ *     it enqueued has completed on the given stream);
+ *   - all work runs on the CUDA device that is current on the calling thread;
+ *   - there is no CPU fallback: with no usable device the status is
+ *     PMS_E_CUDA.
+ *
+ * Error checks happen in this order (the oracle mirrors it): PMS_E_ARG, then
+ * PMS_E_CHAR, then device errors (PMS_E_CUDA), then PMS_E_TRUNCATED.
+ */
+#ifndef PMS_B200_H
+#define PMS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    PMS_OK = 0,
+    PMS_E_ARG = -1,       /* NULL seqs/count, out_codes NULL with max_out>0,
+                             n<1, t<1, l<1, l>16, l>t, d<0,
+                             lo>hi, plan/shape mismatch */
+    PMS_E_CHAR = -2,      /* a byte outside "ACGTacgt" (incl. 'N') */
+    PMS_E_TOO_LARGE = -3, /* n*t or the packed table exceeds 2^31 bytes */
+    PMS_E_CUDA = -4,      /* no device, allocation/launch/runtime failure */
+    PMS_E_TRUNCATED = -5  /* more motifs than max_out; *count is exact */
+};
+
+#define PMS_MAX_L 16
+
+/* Launch overrides (all 0 = automatic).  Results never depend on them. */
+typedef struct pms_launch {
+    int32_t ctas_per_sm;     /* persistent CTAs per SM (grid = SMs * this)   */
+    int32_t warps_per_cta;   /* warps per CTA                                */
+    int32_t batch;           /* candidates per atomic grab (multiple of 256) */
+    int32_t lanes_per_cand;  /* 16 or 32 lanes per candidate, 0 = pick the
+                                one with less window padding                 */
+    int32_t force_generic;   /* 1 = windows never register-resident          */
+    int32_t reserved[3];
+} pms_launch;
+
+/* Counters and timings of the last execution of a plan. */
+typedef struct pms_stats {
+    double pack_ms;            /* device time of the window pre-pass        */
+    double search_ms;          /* device time of the search kernel          */
+    double total_ms;           /* device time from first to last enqueue    */
+    uint64_t candidates;       /* hi - lo                                    */
+    uint64_t issued_compares;  /* candidate-window Hamming tests the kernel
+                                  issued on real (unpadded) windows          */
+    uint64_t motifs;           /* total motifs found (= *count)              */
+    int32_t grid, block, lanes_per_cand, windows_per_lane, generic,
+            table_in_smem;
+    uint32_t smem_bytes;
+} pms_stats;
+
+/* ---------------------------------------------------------------------
+ * pms_find -- one complete search from HOST buffers (synchronous).
+ *   seqs      host, n*t bytes, row-major (sequence i at seqs + i*t), ASCII
+ *             A/C/G/T in any case.  Read only.
+ *   out_codes host, capacity max_out codes; may be NULL iff max_out == 0.
+ *             On PMS_OK receives *count codes ascending, without duplicates.
+ *             On PMS_E_TRUNCATED its contents are unspecified.
+ *   count     host, required: receives the exact number of motifs (also on
+ *             PMS_E_TRUNCATED, so max_out = 0 works as a size query).
+ * An empty result is PMS_OK with *count = 0; d >= l yields all 4^l codes.
+ * Steps: validate arguments -> H2D copy -> device pre-pass (byte check +
+ * window packing) -> persistent search kernel with in-kernel atomic-append
+ * compaction -> D2H of the count and codes -> host sort.
+ * ------------------------------------------------------------------- */
+int pms_find(const uint8_t *seqs, int32_t n, int32_t t, int32_t l, int32_t d,
+             uint32_t *out_codes, uint64_t max_out, uint64_t *count);
+
+/* pms_find over the candidate-code range [lo, hi) (hi is clipped to 4^l),
+ * with optional launch overrides and stats (each may be NULL).  Range
+ * additivity holds: results over [a,b) and [b,c) concatenate to [a,c). */
+int pms_find_ex(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
+                int32_t d, uint64_t lo, uint64_t hi, const pms_launch *launch,
+                uint32_t *out_codes, uint64_t max_out, uint64_t *count,
+                pms_stats *stats);
+
+/* ---------------------------------------------------------------------
+ * Plans: device-resident, asynchronous form for callers that own device
+ * memory and streams (the Python binding passes torch tensors and
+ * torch.cuda.current_stream()).  A plan holds the packed window table, the
+ * work/result counters and timing events for one (n, t, l, d) shape.
+ * ------------------------------------------------------------------- */
+typedef struct pms_plan pms_plan;
+
+/* Allocates device workspace for the shape.  *plan receives the handle. */
+int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
+                    const pms_launch *launch, pms_plan **plan);
+
+/* Enqueues pre-pass + search on `stream` (a cudaStream_t; NULL = legacy
+ * default stream).  Does not synchronize.
+ *   d_seqs   device, n*t bytes as for pms_find.
+ *   d_out    device, capacity `cap` codes (NULL iff cap == 0): receives the
+ *            first min(total, cap) motif codes in UNSPECIFIED order.
+ *   d_count  device, one uint64: receives the total number of motifs once the
+ *            work completes (also when total > cap).
+ * Byte errors are detected on the device; query them with pms_plan_wait. */
+int pms_plan_execute(pms_plan *plan, const uint8_t *d_seqs, uint64_t lo,
+                     uint64_t hi, uint32_t *d_out, uint64_t cap,
+                     uint64_t *d_count, void *stream);
+
+/* Waits for the plan's last execution; returns PMS_E_CHAR if the pre-pass
+ * saw an invalid byte (the search then did no work and *d_count is 0),
+ * PMS_E_CUDA on a device error, else PMS_OK.  Fills *stats if non-NULL. */
+int pms_plan_wait(pms_plan *plan, pms_stats *stats);
+
+void pms_plan_destroy(pms_plan *plan);
+
+/* ---------------------------------------------------------------------
+ * Integer-pipe roofline microbenchmark (SURVEY 8(d) R_mix): runs the search
+ * kernel's exact per-compare instruction sequence (XOR; XOR-OR fold with
+ * the 16-bit-rotated operands; POPC; 3-way min) on register-resident
+ * windows with no early exit, on every SM, for `iters` candidates per warp.
+ *   compares_per_s   receives compares / second (CUDA-event timed)
+ *   compares_per_clk_sm receives compares / SM-clock / SM, using the SM
+ *                    clock rate the driver reports (may be NULL)
+ *   ms               receives the kernel time (may be NULL)
+ * ------------------------------------------------------------------- */
+int pms_roofline(int32_t iters, double *compares_per_s,
+                 double *compares_per_clk_sm, double *ms);
+
+/* Static description of a status code. */
+const char *pms_strerror(int status);
+
+/* Number of SMs and the opt-in shared memory per block of the current
+ * device (for reporting); PMS_E_CUDA without a device. */
+int pms_device_info(int32_t *sms, int32_t *smem_optin_bytes,
+                    int32_t *clock_khz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMS_B200_H */

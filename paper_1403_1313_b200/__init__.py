@@ -1,0 +1,223 @@
+"""B200-native Skip-Brute-Force planted (l,d) motif search (arxiv 1403.1313).
+
+Thin ctypes binding over ``libpms_b200.so`` (include/pms.h): argument
+marshalling only -- every step of the search runs in the library's CUDA
+kernels.  There is no CPU fallback: if the library is missing or no CUDA
+device is usable, calls raise.  PyTorch is used only by callers that want to
+pass device tensors and streams (``Plan.execute``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._build import LIB, build
+
+OK, E_ARG, E_CHAR, E_TOO_LARGE, E_CUDA, E_TRUNCATED = 0, -1, -2, -3, -4, -5
+MAX_L = 16
+
+__all__ = ["find", "find_ex", "Plan", "Launch", "Stats", "roofline", "device_info", "strerror",
+           "PmsError", "load", "build", "decode_code", "LIB"]
+
+
+class PmsError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        super().__init__(f"{what}: {strerror(status)} (status {status})" if what else
+                         f"{strerror(status)} (status {status})")
+
+
+class Launch(ctypes.Structure):
+    _fields_ = [("ctas_per_sm", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32),
+                ("batch", ctypes.c_int32), ("lanes_per_cand", ctypes.c_int32),
+                ("force_generic", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("pack_ms", ctypes.c_double), ("search_ms", ctypes.c_double),
+                ("total_ms", ctypes.c_double), ("candidates", ctypes.c_uint64),
+                ("issued_compares", ctypes.c_uint64), ("motifs", ctypes.c_uint64),
+                ("grid", ctypes.c_int32), ("block", ctypes.c_int32),
+                ("lanes_per_cand", ctypes.c_int32), ("windows_per_lane", ctypes.c_int32),
+                ("generic", ctypes.c_int32), ("table_in_smem", ctypes.c_int32),
+                ("smem_bytes", ctypes.c_uint32)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libpms_b200.so (built in-tree by build()); raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"{LIB} not built: run paper_1403_1313_b200.build() "
+                              "(nvcc, sm_100a); there is no CPU fallback")
+        lib = ctypes.CDLL(LIB)
+        vp, u8p, u32p, u64p = (ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint8),
+                               ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint64))
+        i32, u64 = ctypes.c_int32, ctypes.c_uint64
+        lib.pms_find.argtypes = [u8p, i32, i32, i32, i32, u32p, u64, u64p]
+        lib.pms_find.restype = ctypes.c_int
+        lib.pms_find_ex.argtypes = [u8p, i32, i32, i32, i32, u64, u64, ctypes.POINTER(Launch),
+                                    u32p, u64, u64p, ctypes.POINTER(Stats)]
+        lib.pms_find_ex.restype = ctypes.c_int
+        lib.pms_plan_create.argtypes = [i32, i32, i32, i32, ctypes.POINTER(Launch),
+                                        ctypes.POINTER(vp)]
+        lib.pms_plan_create.restype = ctypes.c_int
+        lib.pms_plan_execute.argtypes = [vp, vp, u64, u64, vp, u64, vp, vp]
+        lib.pms_plan_execute.restype = ctypes.c_int
+        lib.pms_plan_wait.argtypes = [vp, ctypes.POINTER(Stats)]
+        lib.pms_plan_wait.restype = ctypes.c_int
+        lib.pms_plan_destroy.argtypes = [vp]
+        lib.pms_plan_destroy.restype = None
+        lib.pms_roofline.argtypes = [i32, ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ctypes.c_double)]
+        lib.pms_roofline.restype = ctypes.c_int
+        lib.pms_strerror.argtypes = [ctypes.c_int]
+        lib.pms_strerror.restype = ctypes.c_char_p
+        lib.pms_device_info.argtypes = [ctypes.POINTER(i32)] * 3
+        lib.pms_device_info.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def strerror(status: int) -> str:
+    return load().pms_strerror(int(status)).decode()
+
+
+def _rows(seqs) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(seqs, dtype=np.uint8))
+    if a.ndim != 2:
+        raise ValueError("seqs must be a 2-D uint8 array [n, t]")
+    return a
+
+
+@dataclass
+class FindResult:
+    status: int
+    codes: np.ndarray   # uint32 ascending (valid when status == OK)
+    count: int          # exact number of motifs
+    stats: Stats | None = None
+
+
+def find_ex(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
+            launch: Launch | None = None, max_out: int = 1 << 20,
+            want_stats: bool = True) -> FindResult:
+    """One call of pms_find_ex from host buffers; returns the raw status."""
+    lib = load()
+    a = _rows(seqs)
+    n, t = a.shape
+    if hi is None:
+        hi = (1 << 64) - 1
+    out = np.zeros(max(int(max_out), 1), dtype=np.uint32)
+    cnt = ctypes.c_uint64(0)
+    st = Stats() if want_stats else None
+    status = lib.pms_find_ex(a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), n, t, l, d,
+                             int(lo), int(hi), ctypes.byref(launch) if launch else None,
+                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), int(max_out),
+                             ctypes.byref(cnt), ctypes.byref(st) if st is not None else None)
+    k = min(int(cnt.value), int(max_out)) if status in (OK, E_TRUNCATED) else 0
+    return FindResult(status, out[:k].copy(), int(cnt.value), st)
+
+
+def find(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
+         launch: Launch | None = None) -> np.ndarray:
+    """All motif codes (ascending uint32) of seqs for (l, d); raises PmsError."""
+    cap = 1 << 16
+    while True:
+        r = find_ex(seqs, l, d, lo, hi, launch, max_out=cap, want_stats=False)
+        if r.status == E_TRUNCATED and r.count > cap:
+            cap = r.count
+            continue
+        if r.status != OK:
+            raise PmsError(r.status, "pms_find_ex")
+        return r.codes
+
+
+def decode_code(code: int, l: int) -> str:
+    """Code -> l-mer string (big-endian base 4, A0 C1 G2 T3) for display."""
+    return "".join("ACGT"[(int(code) >> (2 * (l - 1 - j))) & 3] for j in range(l))
+
+
+class Plan:
+    """Device-resident plan (pms_plan_*): enqueue on a torch/CUDA stream."""
+
+    def __init__(self, n: int, t: int, l: int, d: int, launch: Launch | None = None):
+        self._lib = load()
+        self._h = ctypes.c_void_p()
+        self.n, self.t, self.l, self.d = n, t, l, d
+        s = self._lib.pms_plan_create(n, t, l, d, ctypes.byref(launch) if launch else None,
+                                      ctypes.byref(self._h))
+        if s != OK:
+            raise PmsError(s, "pms_plan_create")
+
+    def execute(self, d_seqs_ptr: int, lo: int, hi: int, d_out_ptr: int, cap: int,
+                d_count_ptr: int, stream: int = 0) -> None:
+        s = self._lib.pms_plan_execute(self._h, ctypes.c_void_p(d_seqs_ptr), int(lo), int(hi),
+                                       ctypes.c_void_p(d_out_ptr) if d_out_ptr else None,
+                                       int(cap), ctypes.c_void_p(d_count_ptr),
+                                       ctypes.c_void_p(stream) if stream else None)
+        if s != OK:
+            raise PmsError(s, "pms_plan_execute")
+
+    def execute_tensors(self, seqs, out, count, lo: int = 0, hi: int | None = None,
+                        stream=None) -> None:
+        """torch tensors on the current device: seqs uint8 [n,t], out int32/uint32
+        [cap], count int64 [1]; stream defaults to torch's current stream."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        assert seqs.is_cuda and seqs.dtype == torch.uint8 and seqs.is_contiguous()
+        assert tuple(seqs.shape) == (self.n, self.t)
+        assert count.dtype == torch.int64 and count.numel() >= 1 and count.is_cuda
+        hi = 4 ** self.l if hi is None else hi
+        self.execute(seqs.data_ptr(), lo, hi, out.data_ptr() if out.numel() else 0, out.numel(),
+                     count.data_ptr(), stream.cuda_stream)
+
+    def wait(self) -> tuple[int, Stats]:
+        st = Stats()
+        s = self._lib.pms_plan_wait(self._h, ctypes.byref(st))
+        return s, st
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.pms_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def roofline(iters: int = 1 << 14) -> dict:
+    """R_mix microbenchmark: the search kernel's per-compare sequence at full
+    occupancy with no early exit (pms_roofline)."""
+    a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    s = load().pms_roofline(int(iters), ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
+    if s != OK:
+        raise PmsError(s, "pms_roofline")
+    return dict(compares_per_s=a.value, compares_per_clk_sm_at_max=b.value, ms=c.value)
+
+
+def device_info() -> dict:
+    a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    s = load().pms_device_info(ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
+    if s != OK:
+        raise PmsError(s, "pms_device_info")
+    return dict(sms=a.value, smem_optin=b.value, clock_khz=c.value)

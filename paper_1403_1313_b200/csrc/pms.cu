@@ -1,0 +1,652 @@
+// pms.cu -- B200 (sm_100a) Skip-Brute-Force planted (l,d) motif search:
+// device pre-pass, persistent search kernels, roofline microbenchmark, and
+// the host orchestration behind the C ABI of include/pms.h.
+//
+// Hot path:
+//   a1 validate + stage        host checks (PMS_E_ARG), H2D copy
+//   a2 pack pre-pass           pms_pack_kernel: bytes -> bit-plane window words,
+//                              byte check (PMS_E_CHAR) -- PAPER.md:63, :77
+//   a3 candidate enumeration   64-bit atomic work counter over code ranges;
+//                              the candidate is generated from its index
+//   a4 Hamming test            XOR / XOR-OR fold with rotated operands / POPC
+//   a5 per-sequence match      lanes split windows, warp vote; the skip rule
+//      + skip rule             abandons a candidate at the first sequence with no
+//                              window within d
+//   a6 result append           atomicAdd slot + store ("output the motif")
+//   a7 finish                  D2H count + codes, host sort (ascending codes)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <new>
+
+#include "pms.h"
+#include "pms_device.cuh"
+
+using namespace pms;
+
+namespace {
+
+constexpr int kSub = 256;          // candidates per aligned sub-block (4 low digits)
+constexpr int kBlock = 256;        // threads per CTA (8 warps)
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// bit-plane word of every 4-digit value i (the low 4 digits of a candidate)
+__constant__ uint32_t c_bp256[kSub];
+
+struct SearchArgs {
+    const uint32_t* tab;            // packed table [n][Wp] (global)
+    int n, W, Wp;
+    uint32_t d2;                    // 2*min(d, l): popc(x|rot16(x)) = 2*Hamming
+    unsigned long long lo, hi;      // candidate code range [lo, hi)
+    unsigned long long lo_al;       // lo rounded down to kSub
+    unsigned long long span;        // hi - lo_al
+    int batch;                      // candidates per atomic grab (multiple of kSub)
+    int in_smem;                    // stage the table into shared memory (TMA bulk)
+    uint32_t tab_bytes;
+    DevState* st;
+    unsigned long long* nout;       // result counter (caller's d_count)
+    uint32_t* out;                  // result buffer, capacity cap
+    unsigned long long cap;
+};
+
+// ------------------------------------------------------------------ a2 pre-pass
+// One thread per (sequence i, window k < Wp).  Window k (the length-l
+// substring starting at k, k in [0, W)) is packed into a bit-plane word; rows
+// are padded to Wp (multiple of 32) with copies of window W-1, which cannot
+// change "some window is within d".  Every byte lies in at least one window,
+// so the byte check covers the whole input.
+__global__ void pms_pack_kernel(const uint8_t* __restrict__ seqs, int n, int t, int l, int W,
+                                int Wp, uint32_t* __restrict__ tab, DevState* st) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= (long long)n * Wp) return;
+    const int i = (int)(idx / Wp);
+    const int k = (int)(idx - (long long)i * Wp);
+    const uint8_t* p = seqs + (long long)i * t + min(k, W - 1);
+    uint32_t H = 0, L = 0, bad = 0;
+    for (int j = 0; j < l; ++j) {
+        const uint32_t u = p[j] & 0xDFu;  // upper-case; only 'x'/'X' map to 'X'
+        const uint32_t code = u == 'A' ? 0u : u == 'C' ? 1u : u == 'G' ? 2u : u == 'T' ? 3u : 4u;
+        bad |= code >> 2;
+        H = (H << 1) | ((code >> 1) & 1u);
+        L = (L << 1) | (code & 1u);
+    }
+    tab[idx] = (H << 16) | L;
+    if (bad) atomicOr(&st->bad, 1u);
+}
+
+// ------------------------------------------------------------- shared pieces
+// Stage the packed table into shared memory with one TMA bulk copy per 64 KB,
+// completion tracked by an mbarrier (transaction bytes).
+__device__ __forceinline__ void stage_table(const SearchArgs& a, uint32_t* stab, uint64_t* bar) {
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(bar, a.tab_bytes);
+        constexpr uint32_t kChunk = 65536;
+        for (uint32_t off = 0; off < a.tab_bytes; off += kChunk) {
+            const uint32_t bytes = min(kChunk, a.tab_bytes - off);
+            tma_bulk_g2s(reinterpret_cast<char*>(stab) + off,
+                         reinterpret_cast<const char*>(a.tab) + off, bytes, bar);
+        }
+    }
+    mbar_wait(bar, 0);
+}
+
+// a4+a5 for sequences [i0, n) with the whole warp on one candidate: lanes take
+// windows k = lane, lane+32, ...; one vote per sequence; the first sequence
+// with no window within d abandons the candidate (skip rule).
+__device__ __forceinline__ bool check_sequences(const uint32_t* tab, int i0, int n, int Wp,
+                                                uint32_t cb, uint32_t d2, int lane,
+                                                unsigned long long& scanned) {
+    const uint32_t cr = rot16(cb);
+    for (int i = i0; i < n; ++i) {
+        const uint32_t* row = tab + (size_t)i * Wp;
+        uint32_t m = 0xFFu;
+#pragma unroll 4
+        for (int k = lane; k < Wp; k += 32) {
+            const uint32_t w = row[k];
+            m = min(m, mism2(cb, cr, w, rot16(w)));
+        }
+        ++scanned;
+        if (!__any_sync(kFull, m <= d2)) return false;
+    }
+    return true;
+}
+
+// a6: atomic-append compaction
+__device__ __forceinline__ void append(const SearchArgs& a, uint32_t code) {
+    const unsigned long long slot = atomicAdd(a.nout, 1ull);
+    if (slot < a.cap) a.out[slot] = code;
+}
+
+// -------------------------------------------------- a3-a6 persistent search
+// Register-resident variant.  G lanes per candidate (G = 16: two candidates
+// per warp iteration; G = 32: one); each lane keeps NW windows of sequence 0
+// (k = hl + G*j, clamped to W-1) and their rotations in registers, since
+// sequence 0 is scanned for every candidate.  Survivors of sequence 0 are
+// checked against sequences 1..n-1 from shared memory by the whole warp.
+template <int G, int NW, bool SMEM>
+__global__ void __launch_bounds__(kBlock) pms_search_reg(SearchArgs a) {
+    extern __shared__ __align__(128) uint32_t stab[];
+    __shared__ __align__(8) uint64_t bar;
+    if (*(volatile unsigned int*)&a.st->bad) return;  // invalid input: no work
+    if (SMEM) stage_table(a, stab, &bar);
+    const uint32_t* tab = SMEM ? stab : a.tab;
+
+    constexpr int CPI = 32 / G;  // candidates per warp iteration
+    const int lane = threadIdx.x & 31;
+    const uint32_t half = (G == 32) ? 0u : (uint32_t)(lane / G);
+    const int hl = lane % G;
+    uint32_t w[NW], wr[NW];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+        w[j] = tab[min(hl + G * j, a.W - 1)];
+        wr[j] = rot16(w[j]);
+    }
+    unsigned long long scanned = 0;
+    for (;;) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(&a.st->next, (unsigned long long)a.batch);
+        b = __shfl_sync(kFull, b, 0);
+        if (b >= a.span) break;
+        for (int sb = 0; sb < a.batch; sb += kSub) {
+            const unsigned long long cbase = a.lo_al + b + sb;
+            if (cbase >= a.hi) break;
+            const uint32_t ubp = code_to_bp((uint32_t)cbase);
+            const bool whole = cbase >= a.lo && cbase + kSub <= a.hi;
+            for (int it = 0; it < kSub; it += CPI) {
+                const uint32_t cb = ubp | c_bp256[it] | half;
+                const uint32_t cr = rot16(cb);
+                uint32_t m = 0xFFu;
+#pragma unroll
+                for (int j = 0; j < NW; ++j) m = min(m, mism2(cb, cr, w[j], wr[j]));
+                bool hit = m <= a.d2;
+                if (!whole) {
+                    const unsigned long long code = cbase + it + half;
+                    hit = hit && code >= a.lo && code < a.hi;
+                }
+                const uint32_t bal = __ballot_sync(kFull, hit);
+                if (bal) {
+#pragma unroll
+                    for (int h = 0; h < CPI; ++h) {
+                        const uint32_t hb = (G == 32) ? bal : ((bal >> (16 * h)) & 0xFFFFu);
+                        if (hb) {
+                            const uint32_t cbh = ubp | c_bp256[it] | (uint32_t)h;
+                            if (check_sequences(tab, 1, a.n, a.Wp, cbh, a.d2, lane, scanned) &&
+                                lane == 0)
+                                append(a, (uint32_t)(cbase + it + h));
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (lane == 0 && scanned) atomicAdd(&a.st->extra, scanned);
+}
+
+// Generic variant (any W; table in shared or global memory): the whole warp
+// takes one candidate and scans sequences 0..n-1 with the skip rule.
+template <bool SMEM>
+__global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
+    extern __shared__ __align__(128) uint32_t stab[];
+    __shared__ __align__(8) uint64_t bar;
+    if (*(volatile unsigned int*)&a.st->bad) return;
+    if (SMEM) stage_table(a, stab, &bar);
+    const uint32_t* tab = SMEM ? stab : a.tab;
+    const int lane = threadIdx.x & 31;
+    unsigned long long scanned = 0;
+    for (;;) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(&a.st->next, (unsigned long long)a.batch);
+        b = __shfl_sync(kFull, b, 0);
+        if (b >= a.span) break;
+        for (int sb = 0; sb < a.batch; sb += kSub) {
+            const unsigned long long cbase = a.lo_al + b + sb;
+            if (cbase >= a.hi) break;
+            const uint32_t ubp = code_to_bp((uint32_t)cbase);
+            for (int it = 0; it < kSub; ++it) {
+                const unsigned long long code = cbase + it;
+                if (code < a.lo || code >= a.hi) continue;
+                if (check_sequences(tab, 0, a.n, a.Wp, ubp | c_bp256[it], a.d2, lane, scanned) &&
+                    lane == 0)
+                    append(a, (uint32_t)code);
+            }
+        }
+    }
+    if (lane == 0 && scanned) atomicAdd(&a.st->extra, scanned);
+}
+
+// ---------------------------------------------------- roofline microbenchmark
+// The exact per-compare sequence of pms_search_reg<G,NW> (same register-
+// resident windows, same candidate generation, same vote), with no early exit
+// and no survivor path: compares/clk/SM of this loop is R_mix.
+template <int G, int NW>
+__global__ void __launch_bounds__(kBlock) pms_roofline_kernel(const uint32_t* __restrict__ tab,
+                                                              int iters, uint32_t d2,
+                                                              unsigned long long* sink) {
+    constexpr int CPI = 32 / G;
+    const int lane = threadIdx.x & 31;
+    const uint32_t half = (G == 32) ? 0u : (uint32_t)(lane / G);
+    const int hl = lane % G;
+    uint32_t w[NW], wr[NW];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+        w[j] = tab[hl + G * j];
+        wr[j] = rot16(w[j]);
+    }
+    uint32_t hits = 0;
+    const uint32_t ubp0 = code_to_bp(blockIdx.x * 65536u + (threadIdx.x >> 5) * 1024u);
+    for (int sb = 0; sb < iters; sb += kSub) {
+        const uint32_t ubp = ubp0 + (uint32_t)sb;  // varies the candidate stream
+        for (int it = 0; it < kSub; it += CPI) {
+            const uint32_t cb = ubp | c_bp256[it] | half;
+            const uint32_t cr = rot16(cb);
+            uint32_t m = 0xFFu;
+#pragma unroll
+            for (int j = 0; j < NW; ++j) m = min(m, mism2(cb, cr, w[j], wr[j]));
+            hits += __ballot_sync(kFull, m <= d2) != 0u;
+        }
+    }
+    if (hits == 0xFFFFFFFFu) sink[0] = hits;  // never true; keeps the work live
+}
+
+// ------------------------------------------------------ kernel instance table
+using SearchFn = void (*)(SearchArgs);
+struct RegKernel {
+    int G, NW;
+    SearchFn fn_smem, fn_global;
+};
+#define PMS_NW_LIST(X) \
+    X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10) X(12) X(14) X(16) X(19) X(22) X(25) X(28) \
+    X(31) X(34) X(37) X(40) X(44) X(48)
+#define PMS_REG16(nw) {16, nw, pms_search_reg<16, nw, true>, pms_search_reg<16, nw, false>},
+#define PMS_REG32(nw) {32, nw, pms_search_reg<32, nw, true>, pms_search_reg<32, nw, false>},
+const RegKernel kRegKernels[] = {PMS_NW_LIST(PMS_REG16) PMS_NW_LIST(PMS_REG32)};
+
+bool pick_reg_kernel(int W, int force_g, RegKernel* best) {
+    bool found = false;
+    int best_waste = 0;
+    for (const RegKernel& k : kRegKernels) {
+        if (force_g && k.G != force_g) continue;
+        if (k.G * k.NW < W) continue;
+        const int waste = k.G * k.NW - W;
+        // smallest NW per G is the first that fits (list ascending); prefer less
+        // padding, then G = 32 (half the registers for the same padding)
+        if (!found || waste < best_waste || (waste == best_waste && k.G > best->G)) {
+            *best = k;
+            best_waste = waste;
+            found = true;
+        }
+    }
+    return found;
+}
+
+int ensure_constants() {
+    static thread_local int dev_done[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return PMS_E_CUDA;
+    if (dev_done[dev]) return PMS_OK;
+    uint32_t h[kSub];
+    for (int i = 0; i < kSub; ++i) h[i] = code_to_bp((uint32_t)i);
+    if (cudaMemcpyToSymbol(c_bp256, h, sizeof(h)) != cudaSuccess) return PMS_E_CUDA;
+    dev_done[dev] = 1;
+    return PMS_OK;
+}
+
+}  // namespace
+
+// ========================================================================
+//                                   plan
+// ========================================================================
+struct pms_plan {
+    int n = 0, t = 0, l = 0, d = 0, W = 0, Wp = 0;
+    int dev = 0, sms = 0;
+    pms_launch launch{};
+    uint32_t* d_table = nullptr;
+    DevState* d_state = nullptr;
+    DevState* h_state = nullptr;  // pinned mirror, filled after each execution
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, packed, searched, state copied
+    SearchFn fn = nullptr;
+    int G = 32, NW = 0, generic = 0, in_smem = 0;
+    uint32_t tab_bytes = 0, smem_bytes = 0;
+    int grid = 0, block = kBlock, batch = kSub;
+    unsigned long long last_lo = 0, last_hi = 0;
+    bool executed = false;
+};
+
+namespace {
+
+int check_shape(int32_t n, int32_t t, int32_t l, int32_t d) {
+    if (n < 1 || t < 1 || l < 1 || l > PMS_MAX_L || l > t || d < 0) return PMS_E_ARG;
+    if ((long long)n * t > 0x7FFFFFFFLL) return PMS_E_TOO_LARGE;
+    const long long W = t - l + 1, Wp = (W + 31) / 32 * 32;
+    if (n * Wp * 4 > 0x7FFFFFFFLL) return PMS_E_TOO_LARGE;
+    return PMS_OK;
+}
+
+void destroy_plan(pms_plan* p) {
+    if (!p) return;
+    cudaFree(p->d_table);
+    cudaFree(p->d_state);
+    cudaFreeHost(p->h_state);
+    for (cudaEvent_t e : p->ev)
+        if (e) cudaEventDestroy(e);
+    delete p;
+}
+
+}  // namespace
+
+extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
+                               const pms_launch* launch, pms_plan** plan) {
+    if (!plan) return PMS_E_ARG;
+    *plan = nullptr;
+    int st = check_shape(n, t, l, d);
+    if (st != PMS_OK) return st;
+    pms_plan* p = new (std::nothrow) pms_plan();
+    if (!p) return PMS_E_CUDA;
+    p->n = n; p->t = t; p->l = l; p->d = d;
+    p->W = t - l + 1;
+    p->Wp = (p->W + 31) / 32 * 32;
+    if (launch) p->launch = *launch;
+    int smem_optin = 0;
+    if (cudaGetDevice(&p->dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->dev) !=
+            cudaSuccess ||
+        ensure_constants() != PMS_OK) {
+        destroy_plan(p);
+        return PMS_E_CUDA;
+    }
+    p->tab_bytes = (uint32_t)((size_t)n * p->Wp * 4);
+    const uint32_t static_smem = 64;  // mbarrier + slack
+    p->in_smem = p->tab_bytes + static_smem <= (uint32_t)smem_optin;
+    p->smem_bytes = p->in_smem ? p->tab_bytes : 0;
+
+    RegKernel rk{};
+    const int force_g = (p->launch.lanes_per_cand == 16 || p->launch.lanes_per_cand == 32)
+                            ? p->launch.lanes_per_cand
+                            : 0;
+    if (!p->launch.force_generic && pick_reg_kernel(p->W, force_g, &rk)) {
+        p->fn = p->in_smem ? rk.fn_smem : rk.fn_global;
+        p->G = rk.G; p->NW = rk.NW; p->generic = 0;
+    } else {
+        p->fn = p->in_smem ? pms_search_generic<true> : pms_search_generic<false>;
+        p->G = 32; p->NW = 0; p->generic = 1;
+    }
+    p->block = p->launch.warps_per_cta > 0 ? 32 * std::min(p->launch.warps_per_cta, 32) : kBlock;
+    if (p->block > kBlock) p->block = kBlock;  // __launch_bounds__(256)
+    if (cudaFuncSetAttribute((const void*)p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)p->smem_bytes) != cudaSuccess) {
+        destroy_plan(p);
+        return PMS_E_CUDA;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->fn, p->block,
+                                                      p->smem_bytes) != cudaSuccess ||
+        occ < 1) {
+        destroy_plan(p);
+        return PMS_E_CUDA;
+    }
+    if (p->launch.ctas_per_sm > 0) occ = std::min(occ, (int)p->launch.ctas_per_sm);
+    p->grid = p->sms * occ;
+    if (cudaMalloc(&p->d_table, p->tab_bytes) != cudaSuccess ||
+        cudaMalloc(&p->d_state, sizeof(DevState)) != cudaSuccess ||
+        cudaMallocHost(&p->h_state, sizeof(DevState)) != cudaSuccess) {
+        destroy_plan(p);
+        return PMS_E_CUDA;
+    }
+    for (cudaEvent_t& e : p->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            destroy_plan(p);
+            return PMS_E_CUDA;
+        }
+    *plan = p;
+    return PMS_OK;
+}
+
+extern "C" void pms_plan_destroy(pms_plan* plan) { destroy_plan(plan); }
+
+extern "C" int pms_plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi,
+                                uint32_t* d_out, uint64_t cap, uint64_t* d_count, void* stream) {
+    if (!p || !d_seqs || !d_count || (!d_out && cap > 0)) return PMS_E_ARG;
+    const unsigned long long total = 1ull << (2 * p->l);
+    if (hi > total) hi = total;
+    if (lo > hi) return PMS_E_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned long long lo_al = lo / kSub * kSub;
+    const unsigned long long span = hi - lo_al;
+
+    // batch: aim for >= 8 grabs per warp, multiple of kSub, at most 16 sub-blocks
+    const unsigned long long warps = (unsigned long long)p->grid * (p->block / 32);
+    int batch = p->launch.batch > 0 ? (p->launch.batch + kSub - 1) / kSub * kSub : 0;
+    if (batch == 0) {
+        unsigned long long b = span / (warps * 8);
+        b = (b + kSub - 1) / kSub * kSub;
+        batch = (int)std::min<unsigned long long>(std::max<unsigned long long>(b, kSub), 16 * kSub);
+    }
+    p->batch = batch;
+    p->last_lo = lo;
+    p->last_hi = hi;
+
+    SearchArgs a{};
+    a.tab = p->d_table; a.n = p->n; a.W = p->W; a.Wp = p->Wp;
+    a.d2 = 2u * (uint32_t)std::min(p->d, p->l);
+    a.lo = lo; a.hi = hi; a.lo_al = lo_al; a.span = span; a.batch = batch;
+    a.in_smem = p->in_smem; a.tab_bytes = p->tab_bytes;
+    a.st = p->d_state; a.nout = reinterpret_cast<unsigned long long*>(d_count);
+    a.out = d_out; a.cap = cap;
+
+    if (cudaEventRecord(p->ev[0], s) != cudaSuccess) return PMS_E_CUDA;
+    if (cudaMemsetAsync(p->d_state, 0, sizeof(DevState), s) != cudaSuccess ||
+        cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s) != cudaSuccess)
+        return PMS_E_CUDA;
+    const long long cells = (long long)p->n * p->Wp;
+    pms_pack_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(d_seqs, p->n, p->t, p->l, p->W,
+                                                                     p->Wp, p->d_table, p->d_state);
+    if (cudaGetLastError() != cudaSuccess) return PMS_E_CUDA;
+    if (cudaEventRecord(p->ev[1], s) != cudaSuccess) return PMS_E_CUDA;
+    if (span > 0) {
+        p->fn<<<p->grid, p->block, p->smem_bytes, s>>>(a);
+        if (cudaGetLastError() != cudaSuccess) return PMS_E_CUDA;
+    }
+    if (cudaEventRecord(p->ev[2], s) != cudaSuccess) return PMS_E_CUDA;
+    if (cudaMemcpyAsync(p->h_state, p->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s) !=
+        cudaSuccess)
+        return PMS_E_CUDA;
+    if (cudaEventRecord(p->ev[3], s) != cudaSuccess) return PMS_E_CUDA;
+    p->executed = true;
+    return PMS_OK;
+}
+
+extern "C" int pms_plan_wait(pms_plan* p, pms_stats* stats) {
+    if (!p || !p->executed) return PMS_E_ARG;
+    if (cudaEventSynchronize(p->ev[3]) != cudaSuccess) return PMS_E_CUDA;
+    if (stats) {
+        float pack = 0.f, search = 0.f, tot = 0.f;
+        cudaEventElapsedTime(&pack, p->ev[0], p->ev[1]);
+        cudaEventElapsedTime(&search, p->ev[1], p->ev[2]);
+        cudaEventElapsedTime(&tot, p->ev[0], p->ev[2]);
+        stats->pack_ms = pack;
+        stats->search_ms = search;
+        stats->total_ms = tot;
+        const unsigned long long cands = p->last_hi - p->last_lo;
+        stats->candidates = cands;
+        const unsigned long long W = (unsigned long long)p->W;
+        stats->issued_compares =
+            p->h_state->bad ? 0 : (p->generic ? 0 : cands * W) + p->h_state->extra * W;
+        stats->motifs = 0;
+        stats->grid = p->grid;
+        stats->block = p->block;
+        stats->lanes_per_cand = p->G;
+        stats->windows_per_lane = p->NW;
+        stats->generic = p->generic;
+        stats->table_in_smem = p->in_smem;
+        stats->smem_bytes = p->smem_bytes;
+    }
+    return p->h_state->bad ? PMS_E_CHAR : PMS_OK;
+}
+
+// ========================================================================
+//                              host entry points
+// ========================================================================
+namespace {
+
+struct DevBufs {
+    uint8_t* seqs = nullptr;
+    uint32_t* out = nullptr;
+    uint64_t* count = nullptr;
+    ~DevBufs() {
+        cudaFree(seqs);
+        cudaFree(out);
+        cudaFree(count);
+    }
+};
+
+}  // namespace
+
+extern "C" int pms_find_ex(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d,
+                           uint64_t lo, uint64_t hi, const pms_launch* launch, uint32_t* out_codes,
+                           uint64_t max_out, uint64_t* count, pms_stats* stats) {
+    // a1: argument checks in the documented order
+    if (!seqs || !count || (!out_codes && max_out > 0)) return PMS_E_ARG;
+    int st = check_shape(n, t, l, d);
+    if (st != PMS_OK) return st;
+    const unsigned long long total = 1ull << (2 * l);
+    if (hi > total) hi = total;
+    if (lo > hi) return PMS_E_ARG;
+    *count = 0;
+
+    pms_plan* plan = nullptr;
+    st = pms_plan_create(n, t, l, d, launch, &plan);
+    if (st != PMS_OK) return st;
+    struct PlanGuard {
+        pms_plan* p;
+        ~PlanGuard() { destroy_plan(p); }
+    } guard{plan};
+
+    const unsigned long long cap = std::min<unsigned long long>(max_out, hi - lo);
+    DevBufs b;
+    const size_t nbytes = (size_t)n * t;
+    if (cudaMalloc(&b.seqs, nbytes) != cudaSuccess ||
+        cudaMalloc(&b.count, sizeof(uint64_t)) != cudaSuccess ||
+        (cap > 0 && cudaMalloc(&b.out, cap * sizeof(uint32_t)) != cudaSuccess))
+        return PMS_E_CUDA;
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return PMS_E_CUDA;
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sguard{s};
+
+    if (cudaMemcpyAsync(b.seqs, seqs, nbytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return PMS_E_CUDA;
+    st = pms_plan_execute(plan, b.seqs, lo, hi, b.out, cap, b.count, s);
+    if (st != PMS_OK) return st;
+    uint64_t found = 0;
+    if (cudaMemcpyAsync(&found, b.count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
+        cudaSuccess)
+        return PMS_E_CUDA;
+    st = pms_plan_wait(plan, stats);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return PMS_E_CUDA;
+    if (st != PMS_OK) return st;
+    if (stats) stats->motifs = found;
+    *count = found;
+    if (found > max_out) return PMS_E_TRUNCATED;
+    // a7: D2H of the codes, host sort (ascending code = lexicographic order)
+    if (found > 0) {
+        if (cudaMemcpy(out_codes, b.out, found * sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
+            cudaSuccess)
+            return PMS_E_CUDA;
+        std::sort(out_codes, out_codes + found);
+    }
+    return PMS_OK;
+}
+
+extern "C" int pms_find(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d,
+                        uint32_t* out_codes, uint64_t max_out, uint64_t* count) {
+    return pms_find_ex(seqs, n, t, l, d, 0, ~0ull, nullptr, out_codes, max_out, count, nullptr);
+}
+
+extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compares_per_clk_sm,
+                            double* ms) {
+    if (iters < kSub || !compares_per_s) return PMS_E_ARG;
+    iters = iters / kSub * kSub;
+    constexpr int G = 16, NW = 37;  // the (15,4) n=20 t=600 headline shape (W = 586)
+    int dev = 0, sms = 0, clk = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev) != cudaSuccess ||
+        ensure_constants() != PMS_OK)
+        return PMS_E_CUDA;
+    uint32_t h[G * NW];
+    uint32_t x = 0x9E3779B9u;
+    for (int i = 0; i < G * NW; ++i) {  // arbitrary 15-mer windows
+        x = x * 1664525u + 1013904223u;
+        h[i] = code_to_bp(x >> 2);
+    }
+    uint32_t* tab = nullptr;
+    unsigned long long* sink = nullptr;
+    if (cudaMalloc(&tab, sizeof(h)) != cudaSuccess ||
+        cudaMalloc(&sink, sizeof(unsigned long long)) != cudaSuccess) {
+        cudaFree(tab);
+        return PMS_E_CUDA;
+    }
+    cudaMemcpy(tab, h, sizeof(h), cudaMemcpyHostToDevice);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pms_roofline_kernel<G, NW>, kBlock, 0);
+    const int grid = sms * std::max(occ, 1);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    pms_roofline_kernel<G, NW><<<grid, kBlock>>>(tab, kSub, 8u, sink);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0);
+        pms_roofline_kernel<G, NW><<<grid, kBlock>>>(tab, iters, 8u, sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, e1);
+        best = std::min(best, t);
+    }
+    const cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(tab);
+    cudaFree(sink);
+    if (err != cudaSuccess) return PMS_E_CUDA;
+    // compares per launch: warps * (iters / CPI) iterations * 32 lanes * NW slots
+    const double warps = (double)grid * (kBlock / 32);
+    const double cmp = warps * ((double)iters / (32 / G)) * 32.0 * NW;
+    *compares_per_s = cmp / (best * 1e-3);
+    if (compares_per_clk_sm) *compares_per_clk_sm = *compares_per_s / ((double)sms * clk * 1e3);
+    if (ms) *ms = best;
+    return PMS_OK;
+}
+
+extern "C" const char* pms_strerror(int status) {
+    switch (status) {
+        case PMS_OK: return "ok";
+        case PMS_E_ARG: return "invalid argument";
+        case PMS_E_CHAR: return "byte outside ACGTacgt in the input";
+        case PMS_E_TOO_LARGE: return "input too large";
+        case PMS_E_CUDA: return "CUDA device error (no device, allocation, launch or runtime)";
+        case PMS_E_TRUNCATED: return "more motifs than max_out (count is exact)";
+        default: return "unknown status";
+    }
+}
+
+extern "C" int pms_device_info(int32_t* sms, int32_t* smem_optin_bytes, int32_t* clock_khz) {
+    int dev = 0, a = 0, b = 0, c = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&a, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&b, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&c, cudaDevAttrClockRate, dev) != cudaSuccess)
+        return PMS_E_CUDA;
+    if (sms) *sms = a;
+    if (smem_optin_bytes) *smem_optin_bytes = b;
+    if (clock_khz) *clock_khz = c;
+    return PMS_OK;
+}

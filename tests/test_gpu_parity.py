@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+All integer work, so the bar is bit-exact: identical sorted uint32 code sets,
+identical counts and statuses.  Full BASELINE.json sizes compare against
+golden sets written by scripts/make_golden.py (oracle only); the rest run
+the oracle live on the same seeded inputs.
+"""
+from __future__ import annotations
+
+import glob
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import fmgen
+import paper_1403_1313_b200 as pms
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: GPU tests must run on the B200 box")
+    pms.build()
+    pms.load()
+
+
+def gpu(seqs, l, d, **kw):
+    r = pms.find_ex(seqs, l, d, max_out=kw.pop("max_out", 1 << 22), **kw)
+    return r
+
+
+def assert_same(seqs, l, d, orc, lo=0, hi=None, launch=None):
+    want = orc.find(seqs, l, d, lo=lo, hi=hi)
+    got = gpu(seqs, l, d, lo=lo, hi=hi, launch=launch)
+    assert got.status == want.status, (got.status, want.status)
+    assert got.count == want.count
+    assert got.codes.tolist() == want.codes.tolist()
+    return got, want
+
+
+# ------------------------------------------------------------- tiny / random
+
+def test_tiny_random_instances(orc):
+    rng = random.Random(2024)
+    for trial in range(80):
+        l = rng.randint(1, 8)
+        n = rng.randint(1, 5)
+        t = rng.randint(l, 70)
+        d = rng.randint(0, min(3, l))
+        s = fmgen.random_sequences(n, t, 500 + trial)
+        assert_same(s, l, d, orc)
+
+
+def test_planted_small_configs(orc):
+    for seed in range(10):
+        s, rec = fmgen.generate_fm(8, 120, 8, 2, seed)
+        got, _ = assert_same(s, 8, 2, orc)
+        code = int("".join(str("ACGT".index(c)) for c in rec.consensus), 4)
+        assert code in set(got.codes.tolist())
+
+
+@pytest.mark.parametrize("W", [1, 2, 15, 16, 17, 31, 32, 33, 63, 64, 65, 97, 255, 586, 600, 769,
+                               985, 1537, 2100])
+def test_window_counts_and_padding(orc, W):
+    """Ragged W around the 16/32-lane tiles, the register-resident limits
+    (16*48, 32*48) and the generic kernel beyond them."""
+    l, d = 7, 2
+    t = W + l - 1
+    n = 3 if W < 1000 else 2
+    s, _ = fmgen.generate_fm(n, t, l, d, W)
+    assert_same(s, l, d, orc)
+
+
+@pytest.mark.parametrize("l,d", [(1, 0), (1, 1), (2, 0), (2, 1), (3, 1), (4, 0), (5, 2), (8, 8),
+                                 (8, 20), (12, 4)])
+def test_l_and_d_edges(orc, l, d):
+    s = fmgen.random_sequences(4, 40, l * 10 + d)
+    assert_same(s, l, d, orc)
+
+
+def test_d_at_least_l_all_codes():
+    s = fmgen.random_sequences(3, 30, 1)
+    for l, d in [(6, 6), (7, 9)]:
+        r = gpu(s, l, d)
+        assert r.status == 0 and r.codes.tolist() == list(range(4 ** l))
+
+
+def test_t_equals_l_closed_form():
+    # n=1, t=l: the Hamming ball, |Ball(15,4)| = 123,841; (16,5) = 1,225,093
+    for l, d, want in [(8, 2, 277), (15, 4, 123841), (16, 5, 1225093)]:
+        s = fmgen.random_sequences(1, l, l)
+        r = gpu(s, l, d)
+        assert r.status == 0 and r.count == want
+
+
+def test_identical_and_homopolymer_sequences(orc):
+    s = np.tile(fmgen.random_sequences(1, 50, 3), (4, 1))
+    assert_same(s, 6, 0, orc)
+    assert_same(s, 6, 1, orc)
+    h = np.full((3, 30), ord("G"), np.uint8)
+    assert_same(h, 5, 1, orc)
+
+
+def test_lowercase_and_invalid_bytes(orc):
+    s = fmgen.random_sequences(3, 40, 9)
+    low = np.frombuffer(bytes(s).lower(), dtype=np.uint8).reshape(s.shape).copy()
+    a = gpu(s, 6, 1)
+    b = gpu(low, 6, 1)
+    assert a.codes.tolist() == b.codes.tolist() == orc.find(s, 6, 1).codes.tolist()
+    for bad_byte in (ord("N"), 0, ord("U"), 0xC1):
+        bad = s.copy()
+        bad[2, 39] = bad_byte
+        assert gpu(bad, 6, 1).status == pms.E_CHAR == orc.find(bad, 6, 1).status
+    bad = s.copy()
+    bad[0, 0] = ord("x")
+    assert gpu(bad, 6, 1).status == pms.E_CHAR
+
+
+def test_truncation_and_size_query(orc):
+    s = fmgen.random_sequences(1, 12, 3)
+    full = gpu(s, 5, 2)
+    assert full.status == 0 and full.count > 20
+    q = gpu(s, 5, 2, max_out=0)
+    assert q.status == pms.E_TRUNCATED and q.count == full.count
+    tr = gpu(s, 5, 2, max_out=7)
+    assert tr.status == pms.E_TRUNCATED and tr.count == full.count
+    ok = gpu(s, 5, 2, max_out=full.count)
+    assert ok.status == 0 and ok.codes.tolist() == full.codes.tolist()
+    assert full.codes.tolist() == orc.find(s, 5, 2).codes.tolist()
+
+
+def test_ranges_and_additivity(orc):
+    s, _ = fmgen.generate_fm(5, 60, 7, 1, 4)
+    full = gpu(s, 7, 1).codes.tolist()
+    for lo, hi in [(0, 0), (0, 1), (1, 255), (255, 257), (300, 5000), (4095, 4 ** 7),
+                   (16383, 16384)]:
+        assert_same(s, 7, 1, orc, lo=lo, hi=hi)
+    for cut in (0, 1, 777, 8192, 16384):
+        a = gpu(s, 7, 1, lo=0, hi=cut).codes.tolist()
+        b = gpu(s, 7, 1, lo=cut, hi=4 ** 7).codes.tolist()
+        assert a + b == full
+
+
+def test_launch_configuration_invariance():
+    s, _ = fmgen.generate_fm(20, 600, 11, 3, 1)
+    base = gpu(s, 11, 3).codes.tolist()
+    for kw in [dict(lanes_per_cand=16), dict(lanes_per_cand=32), dict(force_generic=1),
+               dict(ctas_per_sm=1, warps_per_cta=1), dict(batch=256), dict(batch=4096),
+               dict(warps_per_cta=3, batch=512)]:
+        L = pms.Launch(**kw)
+        for _ in range(2):  # determinism across repeated runs
+            assert gpu(s, 11, 3, launch=L).codes.tolist() == base, kw
+
+
+def test_table_in_global_memory(orc):
+    # n * Wp * 4 = 100 * 608 * 4 = 243,200 B > 227 KB opt-in smem -> global table
+    s, _ = fmgen.generate_fm(100, 600, 9, 2, 5)
+    got, _ = assert_same(s, 9, 2, orc)
+    assert got.stats.table_in_smem == 0
+    got = gpu(s, 9, 2, launch=pms.Launch(force_generic=1))
+    assert got.codes.tolist() == orc.find(s, 9, 2).codes.tolist()
+
+
+def test_l16_subranges(orc):
+    """l = 16 fills the uint32 code space: u64 counters and loop bounds."""
+    s, rec = fmgen.generate_fm(3, 20, 16, 5, 16)
+    cons = int("".join(str("ACGT".index(c)) for c in rec.consensus), 4)
+    for lo, hi in [(0, 1 << 20), (cons - (1 << 19), cons + (1 << 19)),
+                   ((1 << 32) - (1 << 20), 1 << 32)]:
+        lo, hi = max(lo, 0), min(hi, 1 << 32)
+        assert_same(s, 16, 5, orc, lo=lo, hi=hi)
+    full = gpu(s, 16, 5, max_out=1 << 26)
+    assert full.status == 0 and cons in set(full.codes.tolist())
+    pick = random.Random(0).sample(full.codes.tolist(), 50)
+    for c in pick:
+        assert orc.verify_motif(s, 16, 5, c)
+
+
+def test_plan_api_with_torch_tensors(orc):
+    import torch
+    s, _ = fmgen.generate_fm(20, 600, 9, 2, 2)
+    dev = torch.device("cuda:0")
+    seqs = torch.from_numpy(s).to(dev)
+    out = torch.zeros(1 << 16, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.Stream()
+    with pms.Plan(20, 600, 9, 2) as plan:
+        with torch.cuda.stream(stream):
+            plan.execute_tensors(seqs, out, cnt)
+        status, st = plan.wait()
+        assert status == 0
+        n = int(cnt.item())
+        got = sorted(out[:n].cpu().numpy().astype(np.uint32).tolist())
+        assert got == orc.find(s, 9, 2).codes.tolist()
+        # re-execute the same plan on a range
+        with torch.cuda.stream(stream):
+            plan.execute_tensors(seqs, out, cnt, lo=1000, hi=200000)
+        status, st = plan.wait()
+        n = int(cnt.item())
+        got = sorted(out[:n].cpu().numpy().astype(np.uint32).tolist())
+        assert got == orc.find(s, 9, 2, lo=1000, hi=200000).codes.tolist()
+        assert st.candidates == 199000
+        bad = seqs.clone()
+        bad[3, 3] = ord("N")
+        with torch.cuda.stream(stream):
+            plan.execute_tensors(bad, out, cnt)
+        status, _ = plan.wait()
+        assert status == pms.E_CHAR and int(cnt.item()) == 0
+
+
+# ------------------------------------------------- BASELINE.json full sizes
+
+GOLDEN_FILES = sorted(glob.glob(os.path.join(GOLDEN, "bj*_seed*.json")))
+
+
+@pytest.mark.parametrize("path", GOLDEN_FILES, ids=[os.path.basename(p) for p in GOLDEN_FILES])
+def test_baseline_configs_against_golden(orc, path):
+    g = json.load(open(path))
+    s, rec = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
+    assert rec.consensus == g["consensus"]  # the generator reproduces the golden input
+    r = gpu(s, g["l"], g["d"])
+    assert r.status == 0
+    assert r.count == g["count"]
+    assert r.codes.tolist() == g["codes"]
+    # work counters: the kernel scans whole sequences, so it issues at least C_alg
+    assert r.stats.issued_compares >= g["c_alg"]
+    for c in r.codes.tolist():
+        assert orc.verify_motif(s, g["l"], g["d"], c)
