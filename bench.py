@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- BASELINE.json metric on B200: candidate l-mers/s and window
+compares/s of the skip-BF search at (15,4), n=20, t=600, plus the integer-pipe
+roofline fraction, the end-to-end C-ABI number and the CPU oracle baseline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A step = one pass of the whole hot path (device pre-pass + persistent search
+over all 4^15 candidates + result compaction) on one FM instance already
+resident in HBM.  With --gpus N (torchrun, one rank per GPU) every rank solves
+its own independent instance (seed 1 + rank): weak scaling, no data-path
+collective.  `--impl reference` times the CPU oracle (oracle/, the paper's
+static-partition threads) on the host cores over a bounded candidate sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import fmgen  # noqa: E402
+
+WORKLOAD = fmgen.BASELINE_CONFIGS[3]  # (15,4) n=20 t=600 -- BASELINE.json configs[3]
+METRIC = "candidate l-mers/s & window compares/s at (15,4) n=20 t=600; INT-pipe % roofline"
+POPC_PER_CLK_SM = 16  # POPC issue rate per SM per clock (B200; measured ~15 by the probe)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during a region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [x for x in sm if x > 0.5 * mx] if mx else sm
+        med = float(np.median(loaded)) if loaded else None
+        return {"sm_mhz": med, "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- helpers
+def golden_c_alg(seed: int):
+    p = os.path.join(ROOT, "tests", "golden", f"bj3_seed{seed}.json")
+    if os.path.exists(p):
+        g = json.load(open(p))
+        return g["c_alg"], g["codes"]
+    return None, None
+
+
+def dist_setup(n_gpus: int):
+    if n_gpus <= 1 and "RANK" not in os.environ:
+        return 0, 1, 0
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", n_gpus))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    return rank, world, local
+
+
+def oracle_sample(l: int, d: int, seqs, seconds: float, lo_frac: float = 0.5):
+    """Time the CPU oracle over a contiguous candidate range sized for ~seconds."""
+    import oracle
+    oracle.build()
+    cores = oracle.default_threads()
+    lo = int(4 ** l * lo_frac)
+    n = 1 << 14
+    r = oracle.find(seqs, l, d, lo=lo, hi=lo + n, threads=cores)  # calibration
+    t0 = time.perf_counter()
+    r = oracle.find(seqs, l, d, lo=lo, hi=lo + n, threads=cores)
+    dt = time.perf_counter() - t0
+    n = int(min(4 ** l - lo, max(n, n * seconds / max(dt, 1e-4))))
+    return lo, n, cores
+
+
+def run_reference(args) -> int:
+    rank, world, _ = dist_setup(args.gpus)
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    l, d = WORKLOAD["l"], WORKLOAD["d"]
+    seqs, _ = fmgen.generate_fm(WORKLOAD["n"], WORKLOAD["t"], l, d, args.seed)
+    lo, n, cores = oracle_sample(l, d, seqs, args.ref_seconds)
+    times, work = [], 0
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = oracle.find(seqs, l, d, lo=lo, hi=lo + n, threads=cores)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            work += r.c_alg
+    tot = sum(times)
+    value = args.steps * n / tot
+    sample = (f"codes [{lo}, {lo + n}) of 4^{l} (contiguous, from 4^{l}/2), "
+              f"{args.steps} timed repetitions after {args.warmup} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "candidates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8 chars (oracle)", "data": "synthetic",
+        "config": {"workload": WORKLOAD["name"] + f" FM seed {args.seed}", "n": WORKLOAD["n"],
+                   "t": WORKLOAD["t"], "l": l, "d": d, "seed": args.seed,
+                   "l2": "n/a (CPU oracle)"},
+        "window_compares_per_s": work / tot,
+        "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": cores,
+                         "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm
+def run_gpu(args) -> int:
+    import torch
+    import paper_1403_1313_b200 as pms
+
+    rank, world, local = dist_setup(args.gpus)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pms.build()
+    pms.load()
+
+    n, t, l, d = WORKLOAD["n"], WORKLOAD["t"], WORKLOAD["l"], WORKLOAD["d"]
+    seed = args.seed + rank
+    seqs_np, rec = fmgen.generate_fm(n, t, l, d, seed)
+    seqs = torch.from_numpy(seqs_np).to(dev)
+    cap = 1 << 20
+    out = torch.zeros(cap, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.Stream(device=dev)
+    plan = pms.Plan(n, t, l, d)
+    total = 4 ** l
+
+    def step():
+        plan.execute_tensors(seqs, out, cnt, 0, total, stream=stream)
+        status, st = plan.wait()
+        if status != 0:
+            raise pms.PmsError(status, "step")
+        return st
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------- timed region
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    search_ms, issued, last = [], 0, None
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)  # L2 flush between timed steps (not timed)
+                evs[i][0].record(stream)
+                last = step()
+                evs[i][1].record(stream)
+                search_ms.append(last.search_ms)
+                issued += last.issued_compares
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    mine = sum(step_ms)
+    tmax = mine
+    if dist:
+        x = torch.tensor([mine], device=dev, dtype=torch.float64)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        tmax = float(x.item())
+    nfound = int(cnt.item())
+    codes = sorted(out[:nfound].cpu().numpy().astype(np.uint32).tolist())
+    c_alg, gold = golden_c_alg(seed)
+    parity = None if gold is None else (codes == gold)
+
+    # ------------------------------------------------ end to end (host buffers)
+    e2e_ms = []
+    for i in range(args.warmup + args.e2e_steps):
+        t0 = time.perf_counter()
+        r = pms.find_ex(seqs_np, l, d, max_out=cap, want_stats=False)
+        dt = time.perf_counter() - t0
+        assert r.status == 0
+        if i >= args.warmup:
+            e2e_ms.append(1e3 * dt)
+    e2e_tot = float(sum(e2e_ms))
+    if dist:
+        x = torch.tensor([e2e_tot], device=dev, dtype=torch.float64)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        e2e_tot = float(x.item())
+
+    # ------------------------------------------------ roofline microbenchmark
+    with ClockSampler(dev.index) as clk_rm:
+        rm = pms.roofline(1 << 15)
+    cs = clk.summary()
+    if dist:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+
+    search_avg = float(np.mean(search_ms))
+    cands_per_s = world * args.steps * total / (tmax * 1e-3)
+    alg_per_launch = c_alg if c_alg is not None else None
+    achieved = (alg_per_launch / (search_avg * 1e-3)) if alg_per_launch else None
+    sm_mhz = cs["sm_mhz"] or 1965.0
+    sms = pms.device_info()["sms"]
+    peak_popc = POPC_PER_CLK_SM * sms * sm_mhz * 1e6
+    issued_rate = issued / args.steps / (search_avg * 1e-3)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "search_kernel_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        import oracle
+        lo, ns, cores = oracle_sample(l, d, seqs_np, args.cpu_seconds)
+        t0 = time.perf_counter()
+        rr = oracle.find(seqs_np, l, d, lo=lo, hi=lo + ns, threads=cores)
+        dt = time.perf_counter() - t0
+        cpu = {"value": ns / dt, "unit": "candidates/s", "cores": cores, "kind": "oracle",
+               "sample": f"codes [{lo}, {lo + ns}) of 4^{l} (contiguous from 4^{l}/2), one run",
+               "window_compares_per_s": rr.c_alg / dt}
+
+    line = {
+        "metric": METRIC, "value": cands_per_s, "unit": "candidates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmax / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic",
+        "config": {"workload": WORKLOAD["name"] + " FM (BASELINE.json configs[3])",
+                   "n": n, "t": t, "l": l, "d": d,
+                   "seeds": [args.seed + r for r in range(world)],
+                   "l2": "flushed between timed steps (256 MiB write, untimed)",
+                   "kernel": {"grid": last.grid, "block": last.block,
+                              "lanes_per_cand": last.lanes_per_cand,
+                              "windows_per_lane": last.windows_per_lane,
+                              "table_in_smem": last.table_in_smem,
+                              "smem_bytes": last.smem_bytes}},
+        "window_compares_per_s": (world * c_alg / (tmax * 1e-3 / args.steps)) if c_alg else None,
+        "issued_compares_per_s": issued_rate,
+        "search_kernel_ms": search_avg, "pack_kernel_ms": float(last.pack_ms),
+        "motifs": nfound, "parity_vs_golden": parity,
+        "roofline": {"bound": "alu", "achieved": achieved / 1e9 if achieved else None,
+                     "peak": peak_popc / 1e9, "unit": "Gcompares/s",
+                     "frac": (achieved / peak_popc) if achieved else None,
+                     "traffic": traffic,
+                     "peak_basis": f"POPC {POPC_PER_CLK_SM}/clk/SM x {sms} SMs x {sm_mhz:.0f} MHz "
+                                   "(median SM clock in the timed region)",
+                     "achieved_basis": "oracle C_alg (first-match window compares) of this "
+                                       "instance / mean search-kernel event time",
+                     "r_mix": rm["compares_per_s"] / 1e9,
+                     "frac_of_r_mix": (achieved / rm["compares_per_s"]) if achieved else None,
+                     "issued_frac_of_r_mix": issued_rate / rm["compares_per_s"],
+                     "r_mix_clocks": clk_rm.summary()},
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * args.e2e_steps * total / (e2e_tot * 1e-3),
+                "unit": "candidates/s", "h2d_bytes_per_step": n * t,
+                "d2h_bytes_per_step": 8 + 4 * nfound + 32,
+                "path": "pms_find_ex from host buffers (plan create, H2D, kernels, D2H, sort)"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": cs,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=5.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: the contract asks for >= 3 warm-up steps")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
