@@ -60,7 +60,12 @@ typedef struct pms_launch {
     int32_t lanes_per_cand;  /* 16 or 32 lanes per candidate, 0 = pick the
                                 one with less window padding                 */
     int32_t force_generic;   /* 1 = windows never register-resident          */
-    int32_t reserved[3];
+    int32_t grid_ctas;       /* total persistent CTAs (overrides ctas_per_sm;
+                                the "workers" of the paper's Fig. 3/4 sweep)  */
+    int32_t no_skip;         /* 1 = plain brute force (PAPER.md:63 before the
+                                "enhanced version"): every candidate scans all
+                                n sequences; same result, n*W compares each  */
+    int32_t reserved[1];
 } pms_launch;
 
 /* Counters and timings of the last execution of a plan. */

@@ -33,7 +33,8 @@ class PmsError(RuntimeError):
 class Launch(ctypes.Structure):
     _fields_ = [("ctas_per_sm", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32),
                 ("batch", ctypes.c_int32), ("lanes_per_cand", ctypes.c_int32),
-                ("force_generic", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("force_generic", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
+                ("no_skip", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class Stats(ctypes.Structure):

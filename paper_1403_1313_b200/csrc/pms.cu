@@ -44,6 +44,7 @@ struct SearchArgs {
     unsigned long long span;        // hi - lo_al
     int batch;                      // candidates per atomic grab (multiple of kSub)
     int in_smem;                    // stage the table into shared memory (TMA bulk)
+    int skip;                       // 1 = skip rule (skip-BF); 0 = plain brute force
     uint32_t tab_bytes;
     DevState* st;
     unsigned long long* nout;       // result counter (caller's d_count)
@@ -99,8 +100,9 @@ __device__ __forceinline__ void stage_table(const SearchArgs& a, uint32_t* stab,
 // with no window within d abandons the candidate (skip rule).
 __device__ __forceinline__ bool check_sequences(const uint32_t* tab, int i0, int n, int Wp,
                                                 uint32_t cb, uint32_t d2, int lane,
-                                                unsigned long long& scanned) {
+                                                unsigned long long& scanned, bool skip = true) {
     const uint32_t cr = rot16(cb);
+    bool all = true;
     for (int i = i0; i < n; ++i) {
         const uint32_t* row = tab + (size_t)i * Wp;
         uint32_t m = 0xFFu;
@@ -110,9 +112,12 @@ __device__ __forceinline__ bool check_sequences(const uint32_t* tab, int i0, int
             m = min(m, mism2(cb, cr, w, rot16(w)));
         }
         ++scanned;
-        if (!__any_sync(kFull, m <= d2)) return false;
+        if (!__any_sync(kFull, m <= d2)) {
+            all = false;
+            if (skip) return false;  // skip rule: abandon at the first failing sequence
+        }
     }
-    return true;
+    return all;
 }
 
 // a6: atomic-append compaction
@@ -187,7 +192,8 @@ __global__ void __launch_bounds__(kBlock) pms_search_reg(SearchArgs a) {
 }
 
 // Generic variant (any W; table in shared or global memory): the whole warp
-// takes one candidate and scans sequences 0..n-1 with the skip rule.
+// takes one candidate and scans sequences 0..n-1 with the skip rule (or, with
+// a.skip == 0, without it: the plain brute force the skip rule enhances).
 template <bool SMEM>
 __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
     extern __shared__ __align__(128) uint32_t stab[];
@@ -209,7 +215,8 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
             for (int it = 0; it < kSub; ++it) {
                 const unsigned long long code = cbase + it;
                 if (code < a.lo || code >= a.hi) continue;
-                if (check_sequences(tab, 0, a.n, a.Wp, ubp | c_bp256[it], a.d2, lane, scanned) &&
+                if (check_sequences(tab, 0, a.n, a.Wp, ubp | c_bp256[it], a.d2, lane, scanned,
+                                    a.skip != 0) &&
                     lane == 0)
                     append(a, (uint32_t)code);
             }
@@ -368,7 +375,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     const int force_g = (p->launch.lanes_per_cand == 16 || p->launch.lanes_per_cand == 32)
                             ? p->launch.lanes_per_cand
                             : 0;
-    if (!p->launch.force_generic && pick_reg_kernel(p->W, force_g, &rk)) {
+    if (!p->launch.force_generic && !p->launch.no_skip && pick_reg_kernel(p->W, force_g, &rk)) {
         p->fn = p->in_smem ? rk.fn_smem : rk.fn_global;
         p->G = rk.G; p->NW = rk.NW; p->generic = 0;
     } else {
@@ -391,6 +398,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     }
     if (p->launch.ctas_per_sm > 0) occ = std::min(occ, (int)p->launch.ctas_per_sm);
     p->grid = p->sms * occ;
+    if (p->launch.grid_ctas > 0) p->grid = std::min((int)p->launch.grid_ctas, p->grid);
     if (cudaMalloc(&p->d_table, p->tab_bytes) != cudaSuccess ||
         cudaMalloc(&p->d_state, sizeof(DevState)) != cudaSuccess ||
         cudaMallocHost(&p->h_state, sizeof(DevState)) != cudaSuccess) {
@@ -435,6 +443,7 @@ extern "C" int pms_plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo,
     a.d2 = 2u * (uint32_t)std::min(p->d, p->l);
     a.lo = lo; a.hi = hi; a.lo_al = lo_al; a.span = span; a.batch = batch;
     a.in_smem = p->in_smem; a.tab_bytes = p->tab_bytes;
+    a.skip = p->launch.no_skip ? 0 : 1;
     a.st = p->d_state; a.nout = reinterpret_cast<unsigned long long*>(d_count);
     a.out = d_out; a.cap = cap;
 

@@ -234,3 +234,34 @@ def test_baseline_configs_against_golden(orc, path):
     assert r.stats.issued_compares >= g["c_alg"]
     for c in r.codes.tolist():
         assert orc.verify_motif(s, g["l"], g["d"], c)
+
+
+# ------------------------------------------------ plain brute force variant
+
+def test_naive_brute_force_variant(orc):
+    """no_skip = 1: every candidate scans all n sequences (PAPER.md:63 before
+    the skip rule).  Same result; issued compares = (hi-lo) * n * W exactly."""
+    rng = random.Random(77)
+    L = pms.Launch(no_skip=1)
+    for trial in range(20):
+        l = rng.randint(1, 7)
+        n = rng.randint(1, 4)
+        t = rng.randint(l, 50)
+        d = rng.randint(0, 2)
+        s = fmgen.random_sequences(n, t, 900 + trial)
+        got, _ = assert_same(s, l, d, orc, launch=L)
+        assert got.stats.issued_compares == 4 ** l * n * (t - l + 1)
+    s, _ = fmgen.generate_fm(20, 600, 9, 2, 1)
+    got = gpu(s, 9, 2, launch=L)
+    skip = gpu(s, 9, 2)
+    assert got.codes.tolist() == skip.codes.tolist() == orc.find(s, 9, 2).codes.tolist()
+    assert got.stats.issued_compares == 4 ** 9 * 20 * 592
+    assert skip.stats.issued_compares < got.stats.issued_compares
+
+
+def test_grid_size_override():
+    s, _ = fmgen.generate_fm(20, 600, 10, 2, 3)
+    base = gpu(s, 10, 2).codes.tolist()
+    for g in (1, 2, 7, 148):
+        r = gpu(s, 10, 2, launch=pms.Launch(grid_ctas=g))
+        assert r.stats.grid == g and r.codes.tolist() == base
