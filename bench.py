@@ -194,7 +194,8 @@ def run_gpu(args) -> int:
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.Stream(device=dev)
-    plan = pms.Plan(n, t, l, d)
+    algo = {"candidate": pms.ALGO_CANDIDATE, "block": pms.ALGO_BLOCK}[args.algo]
+    plan = pms.Plan(n, t, l, d, pms.Launch(algo=algo))
     total = 4 ** l
 
     def step():
@@ -244,7 +245,8 @@ def run_gpu(args) -> int:
     e2e_ms = []
     for i in range(args.warmup + args.e2e_steps):
         t0 = time.perf_counter()
-        r = pms.find_ex(seqs_np, l, d, max_out=cap, want_stats=False)
+        r = pms.find_ex(seqs_np, l, d, launch=pms.Launch(algo=algo), max_out=cap,
+                        want_stats=False)
         dt = time.perf_counter() - t0
         assert r.status == 0
         if i >= args.warmup:
@@ -297,6 +299,7 @@ def run_gpu(args) -> int:
                    "n": n, "t": t, "l": l, "d": d,
                    "seeds": [args.seed + r for r in range(world)],
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
+                   "algo": args.algo,
                    "kernel": {"grid": last.grid, "block": last.block,
                               "lanes_per_cand": last.lanes_per_cand,
                               "windows_per_lane": last.windows_per_lane,
@@ -337,6 +340,7 @@ def main() -> int:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--algo", choices=["candidate", "block"], default="candidate")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=5.0)

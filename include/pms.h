@@ -65,8 +65,21 @@ typedef struct pms_launch {
     int32_t no_skip;         /* 1 = plain brute force (PAPER.md:63 before the
                                 "enhanced version"): every candidate scans all
                                 n sequences; same result, n*W compares each  */
-    int32_t reserved[1];
+    int32_t algo;            /* PMS_ALGO_*: which kernel family (0 = auto)   */
 } pms_launch;
+
+/* Kernel families (pms_launch.algo).  Every family returns the same set.
+ *   PMS_ALGO_CANDIDATE: one candidate per 16/32 lanes; each candidate-window
+ *     Hamming test is XOR, XOR-OR fold, POPC.
+ *   PMS_ALGO_BLOCK: the 256 candidates that share their first l-4 digits are
+ *     tested together: one XOR/fold/POPC of the shared prefix against a window
+ *     gives the prefix distance p, and the candidates whose last 4 digits lie
+ *     within d-p of the window's last 4 digits (a precomputed Hamming-ball
+ *     bitmask) match that window.  The skip rule applies to the block's alive
+ *     mask: the block is abandoned at the first sequence where no alive
+ *     candidate matches; few survivors fall back to per-candidate checks.
+ *     Needs l >= 5 (else the candidate family runs). */
+enum { PMS_ALGO_AUTO = 0, PMS_ALGO_CANDIDATE = 1, PMS_ALGO_BLOCK = 2 };
 
 /* Counters and timings of the last execution of a plan. */
 typedef struct pms_stats {
@@ -80,6 +93,10 @@ typedef struct pms_stats {
     int32_t grid, block, lanes_per_cand, windows_per_lane, generic,
             table_in_smem;
     uint32_t smem_bytes;
+    int32_t algo;              /* PMS_ALGO_* actually run                    */
+    uint64_t block_scans;      /* PMS_ALGO_BLOCK: (block, sequence) scans;
+                                  each is W prefix compares serving 256
+                                  candidates                                 */
 } pms_stats;
 
 /* ---------------------------------------------------------------------

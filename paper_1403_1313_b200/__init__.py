@@ -17,6 +17,7 @@ import numpy as np
 from ._build import LIB, build
 
 OK, E_ARG, E_CHAR, E_TOO_LARGE, E_CUDA, E_TRUNCATED = 0, -1, -2, -3, -4, -5
+ALGO_AUTO, ALGO_CANDIDATE, ALGO_BLOCK = 0, 1, 2
 MAX_L = 16
 
 __all__ = ["find", "find_ex", "Plan", "Launch", "Stats", "roofline", "device_info", "strerror",
@@ -34,7 +35,7 @@ class Launch(ctypes.Structure):
     _fields_ = [("ctas_per_sm", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32),
                 ("batch", ctypes.c_int32), ("lanes_per_cand", ctypes.c_int32),
                 ("force_generic", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
-                ("no_skip", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
+                ("no_skip", ctypes.c_int32), ("algo", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -44,7 +45,8 @@ class Stats(ctypes.Structure):
                 ("grid", ctypes.c_int32), ("block", ctypes.c_int32),
                 ("lanes_per_cand", ctypes.c_int32), ("windows_per_lane", ctypes.c_int32),
                 ("generic", ctypes.c_int32), ("table_in_smem", ctypes.c_int32),
-                ("smem_bytes", ctypes.c_uint32)]
+                ("smem_bytes", ctypes.c_uint32), ("algo", ctypes.c_int32),
+                ("block_scans", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

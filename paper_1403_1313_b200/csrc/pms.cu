@@ -225,6 +225,174 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
     if (lane == 0 && scanned) atomicAdd(&a.st->extra, scanned);
 }
 
+// ------------------------------------------------- PMS_ALGO_BLOCK search
+// The 256 candidates of a 256-aligned code block share their first l-4 digits
+// (the prefix P) and differ in the last 4 (the suffix x).  For a window w,
+// Hamming(P x, w) = Hamming(P, w[0..l-4)) + Hamming(x, w[l-4..l)), so one
+// XOR / XOR-OR fold / POPC of the prefix against w gives p, and the
+// candidates matching w (distance <= d) are exactly the suffixes inside the
+// Hamming ball of radius d - p around w's suffix: a 256-bit mask read from a
+// table built once per CTA.  The OR of those masks over a sequence's windows
+// is the set of block candidates with a window within d in that sequence
+// (PAPER.md:63); the block's alive mask is ANDed with it, and the block is
+// abandoned at the first sequence that leaves no candidate alive -- the skip
+// rule applied to 256 candidates at once.  Once at most kBlkSwitch candidates
+// remain they are finished one by one (check_sequences).
+constexpr int kBlkS = 4;                    // suffix digits per block
+constexpr int kBlkC = 1 << (2 * kBlkS);     // 256 candidates per block (= kSub)
+constexpr int kBlkWords = kBlkC / 32;       // 8 mask words
+constexpr int kBallWords = kBlkS * kBlkC * kBlkWords;  // radii 0..S-1 (r >= S: all)
+constexpr uint32_t kSfxBits = 0x000F000Fu;  // suffix positions in both planes
+constexpr int kBlkSwitch = 2;
+static_assert(kBlkC == kSub, "blocks are the 256-aligned sub-blocks");
+
+// ball[(r*256 + e)*8 + k] bit b: candidate suffix code x = 32k + b lies within
+// Hamming distance r of the window suffix e = (H4 << 4) | L4 (bit-plane index).
+__device__ __forceinline__ void build_ball(uint32_t* ball) {
+    for (int idx = threadIdx.x; idx < kBallWords; idx += blockDim.x) {
+        const int k = idx % kBlkWords;
+        const int e = (idx / kBlkWords) % kBlkC;
+        const int r = idx / (kBlkWords * kBlkC);
+        const uint32_t eH = (uint32_t)e >> 4, eL = (uint32_t)e & 15u;
+        uint32_t word = 0;
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t x = 32u * k + b;
+            const uint32_t xH = compress_even(x >> 1), xL = compress_even(x);
+            if (__popc((xH ^ eH) | (xL ^ eL)) <= r) word |= 1u << b;
+        }
+        ball[idx] = word;
+    }
+}
+
+// Appends the codes cbase + 32k + b for every set bit b of mask (lane-parallel).
+__device__ __forceinline__ void append_mask(const SearchArgs& a, unsigned long long cbase, int k,
+                                            uint32_t mask, int lane) {
+    if (!mask) return;
+    unsigned long long slot0 = 0;
+    if (lane == 0) slot0 = atomicAdd(a.nout, (unsigned long long)__popc(mask));
+    slot0 = __shfl_sync(kFull, slot0, 0);
+    if ((mask >> lane) & 1u) {
+        const unsigned long long slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+        if (slot < a.cap) a.out[slot] = (uint32_t)(cbase + 32u * k + lane);
+    }
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(kBlock) pms_search_block(SearchArgs a) {
+    extern __shared__ __align__(128) uint32_t stab[];  // [ball][table if SMEM]
+    __shared__ __align__(8) uint64_t bar;
+    if (*(volatile unsigned int*)&a.st->bad) return;
+    uint32_t* ball = stab;
+    uint32_t* tsm = stab + kBallWords;
+    if (SMEM) {  // start the table's TMA bulk copy, build the ball table meanwhile
+        if (threadIdx.x == 0) mbar_init(&bar, 1);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(&bar, a.tab_bytes);
+            constexpr uint32_t kChunk = 65536;
+            for (uint32_t off = 0; off < a.tab_bytes; off += kChunk)
+                tma_bulk_g2s(reinterpret_cast<char*>(tsm) + off,
+                             reinterpret_cast<const char*>(a.tab) + off,
+                             min(kChunk, a.tab_bytes - off), &bar);
+        }
+    }
+    build_ball(ball);
+    __syncthreads();
+    if (SMEM) mbar_wait(&bar, 0);
+    const uint32_t* tab = SMEM ? tsm : a.tab;
+    const int lane = threadIdx.x & 31;
+    unsigned long long scanned = 0, bscans = 0;
+
+    for (;;) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(&a.st->next, (unsigned long long)a.batch);
+        b = __shfl_sync(kFull, b, 0);
+        if (b >= a.span) break;
+        for (int sb = 0; sb < a.batch; sb += kSub) {
+            const unsigned long long cbase = a.lo_al + b + sb;
+            if (cbase >= a.hi) break;
+            const uint32_t cb = code_to_bp((uint32_t)cbase);  // suffix bits are zero
+            uint32_t alive[kBlkWords];
+#pragma unroll
+            for (int k = 0; k < kBlkWords; ++k) {
+                uint32_t m = kFull;
+                const unsigned long long c0 = cbase + 32u * k;
+                if (c0 < a.lo) m = (a.lo - c0 >= 32) ? 0u : m << (a.lo - c0);
+                if (c0 + 32 > a.hi) m &= (a.hi <= c0) ? 0u : (kFull >> (c0 + 32 - a.hi));
+                alive[k] = m;
+            }
+            int i = 0;
+            bool dead = false;
+            for (; i < a.n; ++i) {
+                if (i > 0) {
+                    int na = 0;
+#pragma unroll
+                    for (int k = 0; k < kBlkWords; ++k) na += __popc(alive[k]);
+                    if (na <= kBlkSwitch) break;
+                }
+                uint32_t acc[kBlkWords];
+#pragma unroll
+                for (int k = 0; k < kBlkWords; ++k) acc[k] = 0u;
+                const uint32_t* row = tab + (size_t)i * a.Wp;
+#pragma unroll 2
+                for (int kk = lane; kk < a.Wp; kk += 32) {
+                    const uint32_t w = row[kk];
+                    const uint32_t x = (cb ^ w) & ~kSfxBits;
+                    const uint32_t p2 = __popc(x | rot16(x));  // 2 * prefix distance
+                    if (p2 <= a.d2) {
+                        const int r = (int)(a.d2 - p2) >> 1;     // budget left for the suffix
+                        if (r >= kBlkS) {
+#pragma unroll
+                            for (int k = 0; k < kBlkWords; ++k) acc[k] = kFull;
+                        } else {
+                            const uint32_t e = ((w >> 12) & 0xF0u) | (w & 0xFu);
+                            const uint4* bm =
+                                reinterpret_cast<const uint4*>(ball + (r * kBlkC + e) * kBlkWords);
+                            const uint4 m0 = bm[0], m1 = bm[1];
+                            acc[0] |= m0.x; acc[1] |= m0.y; acc[2] |= m0.z; acc[3] |= m0.w;
+                            acc[4] |= m1.x; acc[5] |= m1.y; acc[6] |= m1.z; acc[7] |= m1.w;
+                        }
+                    }
+                }
+                uint32_t any = 0;
+#pragma unroll
+                for (int k = 0; k < kBlkWords; ++k) {
+                    alive[k] &= __reduce_or_sync(kFull, acc[k]);
+                    any |= alive[k];
+                }
+                ++bscans;
+                if (!any) {  // skip rule: no block candidate matches sequence i
+                    dead = true;
+                    break;
+                }
+            }
+            if (dead) continue;
+            if (i == a.n) {  // every alive candidate matched all n sequences
+#pragma unroll
+                for (int k = 0; k < kBlkWords; ++k) append_mask(a, cbase, k, alive[k], lane);
+                continue;
+            }
+            // few survivors: finish them one by one from sequence i on
+#pragma unroll
+            for (int k = 0; k < kBlkWords; ++k) {
+                uint32_t m = alive[k];
+                while (m) {
+                    const int bit = __ffs(m) - 1;
+                    m &= m - 1;
+                    const uint32_t code = (uint32_t)(cbase + 32u * k + bit);
+                    if (check_sequences(tab, i, a.n, a.Wp, code_to_bp(code), a.d2, lane, scanned) &&
+                        lane == 0)
+                        append(a, code);
+                }
+            }
+        }
+    }
+    if (lane == 0) {
+        if (scanned) atomicAdd(&a.st->extra, scanned);
+        if (bscans) atomicAdd(&a.st->block_scans, bscans);
+    }
+}
+
 // ---------------------------------------------------- roofline microbenchmark
 // The exact per-compare sequence of pms_search_reg<G,NW> (same register-
 // resident windows, same candidate generation, same vote), with no early exit
@@ -316,7 +484,7 @@ struct pms_plan {
     DevState* h_state = nullptr;  // pinned mirror, filled after each execution
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, packed, searched, state copied
     SearchFn fn = nullptr;
-    int G = 32, NW = 0, generic = 0, in_smem = 0;
+    int G = 32, NW = 0, generic = 0, in_smem = 0, algo = PMS_ALGO_CANDIDATE;
     uint32_t tab_bytes = 0, smem_bytes = 0;
     int grid = 0, block = kBlock, batch = kSub;
     unsigned long long last_lo = 0, last_hi = 0;
@@ -368,19 +536,25 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     }
     p->tab_bytes = (uint32_t)((size_t)n * p->Wp * 4);
     const uint32_t static_smem = 64;  // mbarrier + slack
-    p->in_smem = p->tab_bytes + static_smem <= (uint32_t)smem_optin;
-    p->smem_bytes = p->in_smem ? p->tab_bytes : 0;
+    const bool block_algo = p->launch.algo == PMS_ALGO_BLOCK && !p->launch.no_skip && l > kBlkS;
+    const uint32_t ball_bytes = block_algo ? (uint32_t)kBallWords * 4u : 0u;
+    p->in_smem = p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
+    p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0);
 
     RegKernel rk{};
     const int force_g = (p->launch.lanes_per_cand == 16 || p->launch.lanes_per_cand == 32)
                             ? p->launch.lanes_per_cand
                             : 0;
-    if (!p->launch.force_generic && !p->launch.no_skip && pick_reg_kernel(p->W, force_g, &rk)) {
+    if (block_algo) {
+        p->fn = p->in_smem ? pms_search_block<true> : pms_search_block<false>;
+        p->G = 32; p->NW = 0; p->generic = 0; p->algo = PMS_ALGO_BLOCK;
+    } else if (!p->launch.force_generic && !p->launch.no_skip &&
+               pick_reg_kernel(p->W, force_g, &rk)) {
         p->fn = p->in_smem ? rk.fn_smem : rk.fn_global;
-        p->G = rk.G; p->NW = rk.NW; p->generic = 0;
+        p->G = rk.G; p->NW = rk.NW; p->generic = 0; p->algo = PMS_ALGO_CANDIDATE;
     } else {
         p->fn = p->in_smem ? pms_search_generic<true> : pms_search_generic<false>;
-        p->G = 32; p->NW = 0; p->generic = 1;
+        p->G = 32; p->NW = 0; p->generic = 1; p->algo = PMS_ALGO_CANDIDATE;
     }
     p->block = p->launch.warps_per_cta > 0 ? 32 * std::min(p->launch.warps_per_cta, 32) : kBlock;
     if (p->block > kBlock) p->block = kBlock;  // __launch_bounds__(256)
@@ -483,8 +657,16 @@ extern "C" int pms_plan_wait(pms_plan* p, pms_stats* stats) {
         const unsigned long long cands = p->last_hi - p->last_lo;
         stats->candidates = cands;
         const unsigned long long W = (unsigned long long)p->W;
+        // candidate family: W compares per candidate on sequence 0 (register
+        // path) + W per further sequence scanned.  Block family: W prefix
+        // compares per (block, sequence) scan + W per per-candidate scan.
+        const bool seq0_implicit = !p->generic && p->algo == PMS_ALGO_CANDIDATE;
         stats->issued_compares =
-            p->h_state->bad ? 0 : (p->generic ? 0 : cands * W) + p->h_state->extra * W;
+            p->h_state->bad ? 0
+                            : (seq0_implicit ? cands * W : 0) +
+                                  (p->h_state->extra + p->h_state->block_scans) * W;
+        stats->algo = p->algo;
+        stats->block_scans = p->h_state->block_scans;
         stats->motifs = 0;
         stats->grid = p->grid;
         stats->block = p->block;

@@ -265,3 +265,86 @@ def test_grid_size_override():
     for g in (1, 2, 7, 148):
         r = gpu(s, 10, 2, launch=pms.Launch(grid_ctas=g))
         assert r.stats.grid == g and r.codes.tolist() == base
+
+
+# ------------------------------------------------ PMS_ALGO_BLOCK family
+
+BLOCK = pms.Launch(algo=pms.ALGO_BLOCK)
+
+
+def test_block_algo_tiny_random(orc):
+    rng = random.Random(4242)
+    for trial in range(80):
+        l = rng.randint(1, 9)
+        n = rng.randint(1, 5)
+        t = rng.randint(l, 90)
+        d = rng.randint(0, min(4, l))
+        s = fmgen.random_sequences(n, t, 7000 + trial)
+        got, _ = assert_same(s, l, d, orc, launch=BLOCK)
+        assert got.stats.algo == (pms.ALGO_BLOCK if l >= 5 else pms.ALGO_CANDIDATE)
+
+
+def test_block_algo_planted_and_edges(orc):
+    for seed in range(6):
+        s, _ = fmgen.generate_fm(10, 200, 9, 2, seed)
+        assert_same(s, 9, 2, orc, launch=BLOCK)
+    for l, d in [(5, 0), (5, 5), (6, 6), (7, 9), (8, 3), (10, 4), (12, 5)]:
+        s = fmgen.random_sequences(4, 40, l * 3 + d)
+        assert_same(s, l, d, orc, launch=BLOCK)
+    h = np.full((3, 30), ord("T"), np.uint8)
+    assert_same(h, 6, 1, orc, launch=BLOCK)
+    s = np.tile(fmgen.random_sequences(1, 50, 3), (4, 1))
+    assert_same(s, 7, 0, orc, launch=BLOCK)
+    assert_same(s, 7, 2, orc, launch=BLOCK)
+
+
+def test_block_algo_ranges(orc):
+    s, _ = fmgen.generate_fm(5, 60, 7, 1, 4)
+    full = gpu(s, 7, 1, launch=BLOCK).codes.tolist()
+    assert full == orc.find(s, 7, 1).codes.tolist()
+    for lo, hi in [(0, 1), (1, 255), (3, 9), (255, 257), (300, 5000), (4095, 4 ** 7),
+                   (16383, 16384), (100, 100)]:
+        assert_same(s, 7, 1, orc, lo=lo, hi=hi, launch=BLOCK)
+    for cut in (1, 777, 8192):
+        a = gpu(s, 7, 1, lo=0, hi=cut, launch=BLOCK).codes.tolist()
+        b = gpu(s, 7, 1, lo=cut, hi=4 ** 7, launch=BLOCK).codes.tolist()
+        assert a + b == full
+
+
+def test_block_algo_window_counts(orc):
+    for W in (1, 31, 33, 586, 985, 2100):
+        l, d = 8, 2
+        s, _ = fmgen.generate_fm(3, W + l - 1, l, d, W)
+        assert_same(s, l, d, orc, launch=BLOCK)
+
+
+def test_block_algo_global_table_and_l16(orc):
+    s, _ = fmgen.generate_fm(100, 600, 9, 2, 5)
+    got, _ = assert_same(s, 9, 2, orc, launch=BLOCK)
+    assert got.stats.table_in_smem == 0
+    s, rec = fmgen.generate_fm(3, 20, 16, 5, 16)
+    cons = int("".join(str("ACGT".index(c)) for c in rec.consensus), 4)
+    for lo, hi in [(0, 1 << 20), (cons - (1 << 19), cons + (1 << 19)),
+                   ((1 << 32) - (1 << 20), 1 << 32)]:
+        assert_same(s, 16, 5, orc, lo=max(lo, 0), hi=min(hi, 1 << 32), launch=BLOCK)
+    a = gpu(s, 16, 5, max_out=1 << 26, launch=BLOCK)
+    b = gpu(s, 16, 5, max_out=1 << 26)
+    assert a.status == b.status == 0 and a.codes.tolist() == b.codes.tolist()
+
+
+def test_block_algo_launch_invariance():
+    s, _ = fmgen.generate_fm(20, 600, 11, 3, 1)
+    base = gpu(s, 11, 3).codes.tolist()
+    for kw in [dict(), dict(grid_ctas=1), dict(grid_ctas=7), dict(warps_per_cta=3),
+               dict(batch=4096), dict(batch=256)]:
+        L = pms.Launch(algo=pms.ALGO_BLOCK, **kw)
+        assert gpu(s, 11, 3, launch=L).codes.tolist() == base, kw
+
+
+@pytest.mark.parametrize("path", GOLDEN_FILES, ids=[os.path.basename(p) for p in GOLDEN_FILES])
+def test_block_algo_baseline_configs(orc, path):
+    g = json.load(open(path))
+    s, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
+    r = gpu(s, g["l"], g["d"], launch=BLOCK)
+    assert r.status == 0 and r.stats.algo == pms.ALGO_BLOCK
+    assert r.count == g["count"] and r.codes.tolist() == g["codes"]
