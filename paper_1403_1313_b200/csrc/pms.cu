@@ -28,6 +28,10 @@ using namespace pms;
 
 namespace {
 
+#define PMS_NW_LIST(X) \
+    X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10) X(12) X(14) X(16) X(19) X(22) X(25) X(28) \
+    X(31) X(34) X(37) X(40) X(44) X(48)
+
 constexpr int kSub = 256;          // candidates per aligned sub-block (4 low digits)
 constexpr int kBlock = 256;        // threads per CTA (8 warps)
 constexpr uint32_t kFull = 0xFFFFFFFFu;
@@ -277,8 +281,29 @@ __device__ __forceinline__ void append_mask(const SearchArgs& a, unsigned long l
     }
 }
 
-template <bool SMEM>
-__global__ void __launch_bounds__(kBlock) pms_search_block(SearchArgs a) {
+// One window's contribution to a block: p2 = 2 * prefix distance (<= d2 here);
+// OR the suffixes within the remaining budget into acc.
+__device__ __forceinline__ void block_hit(uint32_t p2, uint32_t w, uint32_t d2,
+                                          const uint32_t* ball, uint32_t (&acc)[kBlkWords]) {
+    const int r = (int)(d2 - p2) >> 1;  // budget left for the suffix
+    if (r >= kBlkS) {
+#pragma unroll
+        for (int k = 0; k < kBlkWords; ++k) acc[k] = kFull;
+    } else {
+        const uint32_t e = ((w >> 12) & 0xF0u) | (w & 0xFu);  // window suffix (H4<<4 | L4)
+        const uint4* bm = reinterpret_cast<const uint4*>(ball + (r * kBlkC + e) * kBlkWords);
+        const uint4 m0 = bm[0], m1 = bm[1];
+        acc[0] |= m0.x; acc[1] |= m0.y; acc[2] |= m0.z; acc[3] |= m0.w;
+        acc[4] |= m1.x; acc[5] |= m1.y; acc[6] |= m1.z; acc[7] |= m1.w;
+    }
+}
+
+constexpr int kBlockB = 512;  // max threads per CTA of the block kernel
+
+// NW > 0: lane keeps windows lane + 32j (j < NW) of sequence 0 in registers,
+// pre-masked (suffix bits cleared) and pre-rotated.
+template <bool SMEM, int NW>
+__global__ void __launch_bounds__(kBlockB) pms_search_block(SearchArgs a) {
     extern __shared__ __align__(128) uint32_t stab[];  // [ball][table if SMEM]
     __shared__ __align__(8) uint64_t bar;
     if (*(volatile unsigned int*)&a.st->bad) return;
@@ -301,6 +326,12 @@ __global__ void __launch_bounds__(kBlock) pms_search_block(SearchArgs a) {
     if (SMEM) mbar_wait(&bar, 0);
     const uint32_t* tab = SMEM ? tsm : a.tab;
     const int lane = threadIdx.x & 31;
+    uint32_t wm[NW > 0 ? NW : 1], wmr[NW > 0 ? NW : 1];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+        wm[j] = tab[min(lane + 32 * j, a.W - 1)] & ~kSfxBits;
+        wmr[j] = rot16(wm[j]);
+    }
     unsigned long long scanned = 0, bscans = 0;
 
     for (;;) {
@@ -333,24 +364,41 @@ __global__ void __launch_bounds__(kBlock) pms_search_block(SearchArgs a) {
                 uint32_t acc[kBlkWords];
 #pragma unroll
                 for (int k = 0; k < kBlkWords; ++k) acc[k] = 0u;
+                // pass 1: prefix distance of every window; hits (p2 <= d2, ~1 %
+                // of windows) are recorded in a per-lane bitmask, no branch
                 const uint32_t* row = tab + (size_t)i * a.Wp;
-#pragma unroll 2
-                for (int kk = lane; kk < a.Wp; kk += 32) {
-                    const uint32_t w = row[kk];
-                    const uint32_t x = (cb ^ w) & ~kSfxBits;
-                    const uint32_t p2 = __popc(x | rot16(x));  // 2 * prefix distance
-                    if (p2 <= a.d2) {
-                        const int r = (int)(a.d2 - p2) >> 1;     // budget left for the suffix
-                        if (r >= kBlkS) {
+                const uint32_t cr = rot16(cb);
+                if (NW > 0 && i == 0) {
+                    uint32_t hm = 0;
 #pragma unroll
-                            for (int k = 0; k < kBlkWords; ++k) acc[k] = kFull;
-                        } else {
-                            const uint32_t e = ((w >> 12) & 0xF0u) | (w & 0xFu);
-                            const uint4* bm =
-                                reinterpret_cast<const uint4*>(ball + (r * kBlkC + e) * kBlkWords);
-                            const uint4 m0 = bm[0], m1 = bm[1];
-                            acc[0] |= m0.x; acc[1] |= m0.y; acc[2] |= m0.z; acc[3] |= m0.w;
-                            acc[4] |= m1.x; acc[5] |= m1.y; acc[6] |= m1.z; acc[7] |= m1.w;
+                    for (int j = 0; j < NW; ++j) {
+                        const uint32_t p2 = __popc((cb ^ wm[j]) | (cr ^ wmr[j]));
+                        if (p2 <= a.d2) hm |= 1u << j;
+                    }
+                    // pass 2: the hit windows' suffix masks (window re-read from the table)
+                    while (hm) {
+                        const int j = __ffs(hm) - 1;
+                        hm &= hm - 1;
+                        const uint32_t w = row[lane + 32 * j];  // Wp == 32*NW (padded rows)
+                        const uint32_t x = (cb ^ w) & ~kSfxBits;
+                        block_hit(__popc(x | rot16(x)), w, a.d2, ball, acc);
+                    }
+                } else {
+                    for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
+                        uint32_t hm = 0;
+                        const int kend = min(a.Wp - k0, 32 * 32);
+#pragma unroll 4
+                        for (int j = 0; j < kend / 32; ++j) {
+                            const uint32_t w = row[k0 + lane + 32 * j];
+                            const uint32_t x = (cb ^ w) & ~kSfxBits;
+                            if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;  // 2 * prefix dist
+                        }
+                        while (hm) {
+                            const int j = __ffs(hm) - 1;
+                            hm &= hm - 1;
+                            const uint32_t w = row[k0 + lane + 32 * j];
+                            const uint32_t x = (cb ^ w) & ~kSfxBits;
+                            block_hit(__popc(x | rot16(x)), w, a.d2, ball, acc);
                         }
                     }
                 }
@@ -373,9 +421,12 @@ __global__ void __launch_bounds__(kBlock) pms_search_block(SearchArgs a) {
                 continue;
             }
             // few survivors: finish them one by one from sequence i on
-#pragma unroll
+#pragma unroll 1
             for (int k = 0; k < kBlkWords; ++k) {
-                uint32_t m = alive[k];
+                uint32_t m = alive[0];
+#pragma unroll
+                for (int q = 1; q < kBlkWords; ++q)
+                    if (k == q) m = alive[q];
                 while (m) {
                     const int bit = __ffs(m) - 1;
                     m &= m - 1;
@@ -392,6 +443,15 @@ __global__ void __launch_bounds__(kBlock) pms_search_block(SearchArgs a) {
         if (bscans) atomicAdd(&a.st->block_scans, bscans);
     }
 }
+
+using BlockFn = void (*)(SearchArgs);
+struct BlockKernel {
+    int NW;
+    BlockFn fn_smem, fn_global;
+};
+#define PMS_BLK(nw) {nw, pms_search_block<true, nw>, pms_search_block<false, nw>},
+const BlockKernel kBlockKernels[] = {{0, pms_search_block<true, 0>, pms_search_block<false, 0>},
+                                     PMS_NW_LIST(PMS_BLK)};
 
 // ---------------------------------------------------- roofline microbenchmark
 // The exact per-compare sequence of pms_search_reg<G,NW> (same register-
@@ -433,9 +493,6 @@ struct RegKernel {
     int G, NW;
     SearchFn fn_smem, fn_global;
 };
-#define PMS_NW_LIST(X) \
-    X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10) X(12) X(14) X(16) X(19) X(22) X(25) X(28) \
-    X(31) X(34) X(37) X(40) X(44) X(48)
 #define PMS_REG16(nw) {16, nw, pms_search_reg<16, nw, true>, pms_search_reg<16, nw, false>},
 #define PMS_REG32(nw) {32, nw, pms_search_reg<32, nw, true>, pms_search_reg<32, nw, false>},
 const RegKernel kRegKernels[] = {PMS_NW_LIST(PMS_REG16) PMS_NW_LIST(PMS_REG32)};
@@ -534,9 +591,17 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         destroy_plan(p);
         return PMS_E_CUDA;
     }
+    const bool block_algo = p->launch.algo == PMS_ALGO_BLOCK && !p->launch.no_skip && l > kBlkS;
+    const BlockKernel* bk = &kBlockKernels[0];
+    if (block_algo && !p->launch.force_generic)
+        for (const BlockKernel& k : kBlockKernels)  // sequence 0 register-resident
+            if (k.NW > 0 && 32 * k.NW >= p->W) {
+                bk = &k;
+                p->Wp = 32 * k.NW;  // rows padded to the register tile (re-read on hits)
+                break;
+            }
     p->tab_bytes = (uint32_t)((size_t)n * p->Wp * 4);
     const uint32_t static_smem = 64;  // mbarrier + slack
-    const bool block_algo = p->launch.algo == PMS_ALGO_BLOCK && !p->launch.no_skip && l > kBlkS;
     const uint32_t ball_bytes = block_algo ? (uint32_t)kBallWords * 4u : 0u;
     p->in_smem = p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
     p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0);
@@ -546,8 +611,8 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
                             ? p->launch.lanes_per_cand
                             : 0;
     if (block_algo) {
-        p->fn = p->in_smem ? pms_search_block<true> : pms_search_block<false>;
-        p->G = 32; p->NW = 0; p->generic = 0; p->algo = PMS_ALGO_BLOCK;
+        p->fn = p->in_smem ? bk->fn_smem : bk->fn_global;
+        p->G = 32; p->NW = bk->NW; p->generic = 0; p->algo = PMS_ALGO_BLOCK;
     } else if (!p->launch.force_generic && !p->launch.no_skip &&
                pick_reg_kernel(p->W, force_g, &rk)) {
         p->fn = p->in_smem ? rk.fn_smem : rk.fn_global;
@@ -556,8 +621,10 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         p->fn = p->in_smem ? pms_search_generic<true> : pms_search_generic<false>;
         p->G = 32; p->NW = 0; p->generic = 1; p->algo = PMS_ALGO_CANDIDATE;
     }
-    p->block = p->launch.warps_per_cta > 0 ? 32 * std::min(p->launch.warps_per_cta, 32) : kBlock;
-    if (p->block > kBlock) p->block = kBlock;  // __launch_bounds__(256)
+    const int max_block = p->algo == PMS_ALGO_BLOCK ? kBlockB : kBlock;  // __launch_bounds__
+    p->block = p->launch.warps_per_cta > 0 ? 32 * std::min(p->launch.warps_per_cta, 32)
+                                           : (p->algo == PMS_ALGO_BLOCK ? 384 : kBlock);
+    if (p->block > max_block) p->block = max_block;
     if (cudaFuncSetAttribute((const void*)p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)p->smem_bytes) != cudaSuccess) {
         destroy_plan(p);
