@@ -245,9 +245,10 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
 constexpr int kBlkS = 4;                    // suffix digits per block
 constexpr int kBlkC = 1 << (2 * kBlkS);     // 256 candidates per block (= kSub)
 constexpr int kBlkWords = kBlkC / 32;       // 8 mask words
-constexpr int kBallWords = kBlkS * kBlkC * kBlkWords;  // radii 0..S-1 (r >= S: all)
+constexpr int kBallR = kBlkS + 1;           // radii 0..S (radius S: every suffix)
+constexpr int kBallWords = kBallR * kBlkC * kBlkWords;
 constexpr uint32_t kSfxBits = 0x000F000Fu;  // suffix positions in both planes
-constexpr int kBlkSwitch = 2;
+constexpr int kBlkSwitch = 1;
 static_assert(kBlkC == kSub, "blocks are the 256-aligned sub-blocks");
 
 // ball[(r*256 + e)*8 + k] bit b: candidate suffix code x = 32k + b lies within
@@ -282,20 +283,16 @@ __device__ __forceinline__ void append_mask(const SearchArgs& a, unsigned long l
 }
 
 // One window's contribution to a block: p2 = 2 * prefix distance (<= d2 here);
-// OR the suffixes within the remaining budget into acc.
+// OR the suffixes within the remaining budget r = d - p (clamped to S, where
+// the ball is every suffix) into acc.
 __device__ __forceinline__ void block_hit(uint32_t p2, uint32_t w, uint32_t d2,
                                           const uint32_t* ball, uint32_t (&acc)[kBlkWords]) {
-    const int r = (int)(d2 - p2) >> 1;  // budget left for the suffix
-    if (r >= kBlkS) {
-#pragma unroll
-        for (int k = 0; k < kBlkWords; ++k) acc[k] = kFull;
-    } else {
-        const uint32_t e = ((w >> 12) & 0xF0u) | (w & 0xFu);  // window suffix (H4<<4 | L4)
-        const uint4* bm = reinterpret_cast<const uint4*>(ball + (r * kBlkC + e) * kBlkWords);
-        const uint4 m0 = bm[0], m1 = bm[1];
-        acc[0] |= m0.x; acc[1] |= m0.y; acc[2] |= m0.z; acc[3] |= m0.w;
-        acc[4] |= m1.x; acc[5] |= m1.y; acc[6] |= m1.z; acc[7] |= m1.w;
-    }
+    const int r = min((int)(d2 - p2) >> 1, kBlkS);
+    const uint32_t e = ((w >> 12) & 0xF0u) | (w & 0xFu);  // window suffix (H4<<4 | L4)
+    const uint4* bm = reinterpret_cast<const uint4*>(ball + (r * kBlkC + e) * kBlkWords);
+    const uint4 m0 = bm[0], m1 = bm[1];
+    acc[0] |= m0.x; acc[1] |= m0.y; acc[2] |= m0.z; acc[3] |= m0.w;
+    acc[4] |= m1.x; acc[5] |= m1.y; acc[6] |= m1.z; acc[7] |= m1.w;
 }
 
 constexpr int kBlockB = 512;  // max threads per CTA of the block kernel
@@ -345,12 +342,16 @@ __global__ void __launch_bounds__(kBlockB) pms_search_block(SearchArgs a) {
             const uint32_t cb = code_to_bp((uint32_t)cbase);  // suffix bits are zero
             uint32_t alive[kBlkWords];
 #pragma unroll
-            for (int k = 0; k < kBlkWords; ++k) {
-                uint32_t m = kFull;
-                const unsigned long long c0 = cbase + 32u * k;
-                if (c0 < a.lo) m = (a.lo - c0 >= 32) ? 0u : m << (a.lo - c0);
-                if (c0 + 32 > a.hi) m &= (a.hi <= c0) ? 0u : (kFull >> (c0 + 32 - a.hi));
-                alive[k] = m;
+            for (int k = 0; k < kBlkWords; ++k) alive[k] = kFull;
+            if (cbase < a.lo || cbase + kBlkC > a.hi) {  // edge block of [lo, hi)
+#pragma unroll
+                for (int k = 0; k < kBlkWords; ++k) {
+                    const unsigned long long c0 = cbase + 32u * k;
+                    uint32_t m = kFull;
+                    if (c0 < a.lo) m = (a.lo - c0 >= 32) ? 0u : m << (a.lo - c0);
+                    if (c0 + 32 > a.hi) m &= (a.hi <= c0) ? 0u : (kFull >> (c0 + 32 - a.hi));
+                    alive[k] = m;
+                }
             }
             int i = 0;
             bool dead = false;
@@ -380,6 +381,20 @@ __global__ void __launch_bounds__(kBlockB) pms_search_block(SearchArgs a) {
                         const int j = __ffs(hm) - 1;
                         hm &= hm - 1;
                         const uint32_t w = row[lane + 32 * j];  // Wp == 32*NW (padded rows)
+                        const uint32_t x = (cb ^ w) & ~kSfxBits;
+                        block_hit(__popc(x | rot16(x)), w, a.d2, ball, acc);
+                    }
+                } else if (NW > 0) {  // rows hold exactly 32*NW windows
+                    uint32_t hm = 0;
+#pragma unroll
+                    for (int j = 0; j < NW; ++j) {
+                        const uint32_t x = (cb ^ row[lane + 32 * j]) & ~kSfxBits;
+                        if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
+                    }
+                    while (hm) {
+                        const int j = __ffs(hm) - 1;
+                        hm &= hm - 1;
+                        const uint32_t w = row[lane + 32 * j];
                         const uint32_t x = (cb ^ w) & ~kSfxBits;
                         block_hit(__popc(x | rot16(x)), w, a.d2, ball, acc);
                     }
@@ -420,21 +435,17 @@ __global__ void __launch_bounds__(kBlockB) pms_search_block(SearchArgs a) {
                 for (int k = 0; k < kBlkWords; ++k) append_mask(a, cbase, k, alive[k], lane);
                 continue;
             }
-            // few survivors: finish them one by one from sequence i on
-#pragma unroll 1
-            for (int k = 0; k < kBlkWords; ++k) {
-                uint32_t m = alive[0];
+            // at most kBlkSwitch survivors: finish them one by one from sequence i on
+            uint32_t pick = 0xFFFFFFFFu;  // suffix index of the (single) survivor
 #pragma unroll
-                for (int q = 1; q < kBlkWords; ++q)
-                    if (k == q) m = alive[q];
-                while (m) {
-                    const int bit = __ffs(m) - 1;
-                    m &= m - 1;
-                    const uint32_t code = (uint32_t)(cbase + 32u * k + bit);
-                    if (check_sequences(tab, i, a.n, a.Wp, code_to_bp(code), a.d2, lane, scanned) &&
-                        lane == 0)
-                        append(a, code);
-                }
+            for (int k = kBlkWords - 1; k >= 0; --k)
+                if (alive[k]) pick = 32u * k + (__ffs(alive[k]) - 1);
+            static_assert(kBlkSwitch == 1, "survivor extraction handles one candidate");
+            if (pick != 0xFFFFFFFFu) {
+                const uint32_t code = (uint32_t)(cbase + pick);
+                if (check_sequences(tab, i, a.n, a.Wp, code_to_bp(code), a.d2, lane, scanned) &&
+                    lane == 0)
+                    append(a, code);
             }
         }
     }
@@ -623,7 +634,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     }
     const int max_block = p->algo == PMS_ALGO_BLOCK ? kBlockB : kBlock;  // __launch_bounds__
     p->block = p->launch.warps_per_cta > 0 ? 32 * std::min(p->launch.warps_per_cta, 32)
-                                           : (p->algo == PMS_ALGO_BLOCK ? 384 : kBlock);
+                                           : (p->algo == PMS_ALGO_BLOCK ? kBlockB : kBlock);
     if (p->block > max_block) p->block = max_block;
     if (cudaFuncSetAttribute((const void*)p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)p->smem_bytes) != cudaSuccess) {
@@ -631,9 +642,21 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         return PMS_E_CUDA;
     }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->fn, p->block,
-                                                      p->smem_bytes) != cudaSuccess ||
-        occ < 1) {
+    if (p->algo == PMS_ALGO_BLOCK && p->launch.warps_per_cta <= 0) {
+        // block family: pick the CTA size with the most resident warps per SM
+        int best = 0;
+        for (int blk = kBlockB; blk >= 256; blk -= 64) {
+            int o = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, (const void*)p->fn, blk,
+                                                              p->smem_bytes) != cudaSuccess)
+                continue;
+            if (o * blk > best) { best = o * blk; p->block = blk; occ = o; }
+        }
+    } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->fn, p->block,
+                                                             p->smem_bytes) != cudaSuccess) {
+        occ = 0;
+    }
+    if (occ < 1) {
         destroy_plan(p);
         return PMS_E_CUDA;
     }
