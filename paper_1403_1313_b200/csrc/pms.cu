@@ -44,7 +44,7 @@ struct SearchArgs {
     int n, W, Wp;
     uint32_t d2;                    // 2*min(d, l): popc(x|rot16(x)) = 2*Hamming
     unsigned long long lo, hi;      // candidate code range [lo, hi)
-    unsigned long long lo_al;       // lo rounded down to kSub
+    unsigned long long lo_al;       // lo rounded down to kUnit (1024)
     unsigned long long span;        // hi - lo_al
     int batch;                      // candidates per atomic grab (multiple of kSub)
     int in_smem;                    // stage the table into shared memory (TMA bulk)
@@ -230,83 +230,95 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
 }
 
 // ------------------------------------------------- PMS_ALGO_BLOCK search
-// The 256 candidates of a 256-aligned code block share their first l-4 digits
-// (the prefix P) and differ in the last 4 (the suffix x).  For a window w,
-// Hamming(P x, w) = Hamming(P, w[0..l-4)) + Hamming(x, w[l-4..l)), so one
-// XOR / XOR-OR fold / POPC of the prefix against w gives p, and the
-// candidates matching w (distance <= d) are exactly the suffixes inside the
-// Hamming ball of radius d - p around w's suffix: a 256-bit mask read from a
-// table built once per CTA.  The OR of those masks over a sequence's windows
-// is the set of block candidates with a window within d in that sequence
-// (PAPER.md:63); the block's alive mask is ANDed with it, and the block is
-// abandoned at the first sequence that leaves no candidate alive -- the skip
-// rule applied to 256 candidates at once.  Once at most kBlkSwitch candidates
-// remain they are finished one by one (check_sequences).
-constexpr int kBlkS = 4;                    // suffix digits per block
-constexpr int kBlkC = 1 << (2 * kBlkS);     // 256 candidates per block (= kSub)
-constexpr int kBlkWords = kBlkC / 32;       // 8 mask words
-constexpr int kBallR = kBlkS + 1;           // radii 0..S (radius S: every suffix)
-constexpr int kBallWords = kBallR * kBlkC * kBlkWords;
-constexpr uint32_t kSfxBits = 0x000F000Fu;  // suffix positions in both planes
-constexpr int kBlkSwitch = 1;
-static_assert(kBlkC == kSub, "blocks are the 256-aligned sub-blocks");
+// The 1024 candidates of a 1024-aligned code block share their first l-5
+// digits (the prefix P) and differ in the last 5 (the suffix x).  For a
+// window w, Hamming(P x, w) = Hamming(P, w[0..l-5)) + Hamming(x, w[l-5..l)),
+// so one XOR / XOR-OR fold / POPC of the prefix against w gives p, and the
+// block candidates that match w (distance <= d) are exactly the
+// suffixes within Hamming distance d - p of w's suffix.  Lane L of the warp
+// owns the 32 candidates x = 32L + b: a window with p <= d (a "hit", ~2 % of
+// windows at (15,4)) is broadcast to all lanes (one SHFL), and every lane ORs
+// the matching bits of its own word, read from a 2 KB table.  After a
+// sequence, alive &= acc; the block is abandoned at the first sequence that
+// leaves no candidate alive -- the skip rule on 1024 candidates at once -- and
+// a lone survivor is finished by the whole warp (check_sequences).
+constexpr int kBlkS = 5;                    // suffix digits per block
+constexpr int kBlkC = 1 << (2 * kBlkS);     // 1024 candidates per block
+constexpr uint32_t kSfxBits = 0x001F001Fu;  // suffix positions in both planes
+constexpr int kUnit = kBlkC;                // batch / lo alignment (multiple of kSub)
+static_assert(kUnit % kSub == 0, "batches hold whole 256-candidate sub-blocks");
+// T[r'][h][eH3][eL3] bit b: the suffix digits 2..4 of candidate x = 32L + b
+// (digit 2 = (h, b>>4) with h = L & 1, digit 3 = (b>>2)&3, digit 4 = b&3) are
+// within Hamming distance r' of the window digits 2..4 given as 3-bit planes.
+constexpr int kTR = 3;                      // r' in 0..2 tabulated; r' >= 3: all
+constexpr int kTWords = kTR * 2 * 8 * 8;    // 384 words
 
-// ball[(r*256 + e)*8 + k] bit b: candidate suffix code x = 32k + b lies within
-// Hamming distance r of the window suffix e = (H4 << 4) | L4 (bit-plane index).
-__device__ __forceinline__ void build_ball(uint32_t* ball) {
-    for (int idx = threadIdx.x; idx < kBallWords; idx += blockDim.x) {
-        const int k = idx % kBlkWords;
-        const int e = (idx / kBlkWords) % kBlkC;
-        const int r = idx / (kBlkWords * kBlkC);
-        const uint32_t eH = (uint32_t)e >> 4, eL = (uint32_t)e & 15u;
+__device__ __forceinline__ void build_suffix_table(uint32_t* T) {
+    for (int idx = threadIdx.x; idx < kTWords; idx += blockDim.x) {
+        const uint32_t eL = idx & 7, eH = (idx >> 3) & 7, h = (idx >> 6) & 1;
+        const int r = idx >> 7;
         uint32_t word = 0;
-        for (int b = 0; b < 32; ++b) {
-            const uint32_t x = 32u * k + b;
-            const uint32_t xH = compress_even(x >> 1), xL = compress_even(x);
+        for (uint32_t b = 0; b < 32; ++b) {
+            const uint32_t xH = (h << 2) | (((b >> 3) & 1) << 1) | ((b >> 1) & 1);
+            const uint32_t xL = ((b >> 4) << 2) | (((b >> 2) & 1) << 1) | (b & 1);
             if (__popc((xH ^ eH) | (xL ^ eL)) <= r) word |= 1u << b;
         }
-        ball[idx] = word;
+        T[idx] = word;
     }
-}
-
-// Appends the codes cbase + 32k + b for every set bit b of mask (lane-parallel).
-__device__ __forceinline__ void append_mask(const SearchArgs& a, unsigned long long cbase, int k,
-                                            uint32_t mask, int lane) {
-    if (!mask) return;
-    unsigned long long slot0 = 0;
-    if (lane == 0) slot0 = atomicAdd(a.nout, (unsigned long long)__popc(mask));
-    slot0 = __shfl_sync(kFull, slot0, 0);
-    if ((mask >> lane) & 1u) {
-        const unsigned long long slot = slot0 + __popc(mask & ((1u << lane) - 1u));
-        if (slot < a.cap) a.out[slot] = (uint32_t)(cbase + 32u * k + lane);
-    }
-}
-
-// One window's contribution to a block: p2 = 2 * prefix distance (<= d2 here);
-// OR the suffixes within the remaining budget r = d - p (clamped to S, where
-// the ball is every suffix) into acc.
-__device__ __forceinline__ void block_hit(uint32_t p2, uint32_t w, uint32_t d2,
-                                          const uint32_t* ball, uint32_t (&acc)[kBlkWords]) {
-    const int r = min((int)(d2 - p2) >> 1, kBlkS);
-    const uint32_t e = ((w >> 12) & 0xF0u) | (w & 0xFu);  // window suffix (H4<<4 | L4)
-    const uint4* bm = reinterpret_cast<const uint4*>(ball + (r * kBlkC + e) * kBlkWords);
-    const uint4 m0 = bm[0], m1 = bm[1];
-    acc[0] |= m0.x; acc[1] |= m0.y; acc[2] |= m0.z; acc[3] |= m0.w;
-    acc[4] |= m1.x; acc[5] |= m1.y; acc[6] |= m1.z; acc[7] |= m1.w;
 }
 
 constexpr int kBlockB = 512;  // max threads per CTA of the block kernel
 
+// Hit record of a lane: r = min(d - p, 7) budget left for the suffix, and the
+// window's 5 suffix digits as planes: v = r << 10 | H5 << 5 | L5.
+__device__ __forceinline__ uint32_t hit_record(uint32_t cb, uint32_t w, uint32_t d2) {
+    const uint32_t x = (cb ^ w) & ~kSfxBits;
+    const uint32_t r = min((d2 - __popc(x | rot16(x))) >> 1, 7u);
+    return (r << 10) | (((w >> 16) & 31u) << 5) | (w & 31u);
+}
+
+// Lane-side application of a broadcast hit record to this lane's word.
+__device__ __forceinline__ uint32_t hit_word(uint32_t v, uint32_t lH01, uint32_t lL01, uint32_t lh,
+                                             const uint32_t* T) {
+    const int r = (int)(v >> 10);
+    const uint32_t eH = (v >> 5) & 31u, eL = v & 31u;
+    const int rr = r - __popc(((eH >> 3) ^ lH01) | ((eL >> 3) ^ lL01));  // digits 0,1
+    const uint32_t t = T[(min(max(rr, 0), kTR - 1) << 7) | (lh << 6) | ((eH & 7u) << 3) | (eL & 7u)];
+    return rr < 0 ? 0u : (rr >= kTR ? kFull : t);
+}
+
+// Broadcast every pending hit of every lane (hm bits index the lane's windows
+// row[lane + 32*j]) and OR the matching candidates into each lane's acc.
+__device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uint32_t cb,
+                                           uint32_t d2, int lane, uint32_t lH01, uint32_t lL01,
+                                           uint32_t lh, const uint32_t* T, uint32_t& acc) {
+    for (;;) {
+        uint32_t mine = kFull;
+        if (hm) {
+            const int j = __ffs(hm) - 1;
+            hm &= hm - 1;
+            mine = hit_record(cb, row[lane + 32 * j], d2);
+        }
+        uint32_t who = __ballot_sync(kFull, mine != kFull);
+        if (!who) break;
+        do {
+            const int src = __ffs(who) - 1;
+            who &= who - 1;
+            acc |= hit_word(__shfl_sync(kFull, mine, src), lH01, lL01, lh, T);
+        } while (who);
+    }
+}
+
 // NW > 0: lane keeps windows lane + 32j (j < NW) of sequence 0 in registers,
-// pre-masked (suffix bits cleared) and pre-rotated.
+// pre-masked (suffix bits cleared) and pre-rotated; rows are padded to 32*NW.
 template <bool SMEM, int NW>
-__global__ void __launch_bounds__(kBlockB) pms_search_block(SearchArgs a) {
-    extern __shared__ __align__(128) uint32_t stab[];  // [ball][table if SMEM]
+__global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(SearchArgs a) {
+    extern __shared__ __align__(128) uint32_t stab[];  // [T][table if SMEM]
     __shared__ __align__(8) uint64_t bar;
     if (*(volatile unsigned int*)&a.st->bad) return;
-    uint32_t* ball = stab;
-    uint32_t* tsm = stab + kBallWords;
-    if (SMEM) {  // start the table's TMA bulk copy, build the ball table meanwhile
+    uint32_t* T = stab;
+    uint32_t* tsm = stab + 512;  // keeps the table 2 KB-aligned for the bulk copy
+    if (SMEM) {  // start the table's TMA bulk copy, build the suffix table meanwhile
         if (threadIdx.x == 0) mbar_init(&bar, 1);
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -318,11 +330,15 @@ __global__ void __launch_bounds__(kBlockB) pms_search_block(SearchArgs a) {
                              min(kChunk, a.tab_bytes - off), &bar);
         }
     }
-    build_ball(ball);
+    build_suffix_table(T);
     __syncthreads();
     if (SMEM) mbar_wait(&bar, 0);
     const uint32_t* tab = SMEM ? tsm : a.tab;
     const int lane = threadIdx.x & 31;
+    // this lane's candidate digits 0,1 (planes) and the high bit of digit 2
+    const uint32_t x0 = (uint32_t)lane >> 3, x1 = ((uint32_t)lane >> 1) & 3u;
+    const uint32_t lH01 = ((x0 >> 1) << 1) | (x1 >> 1), lL01 = ((x0 & 1u) << 1) | (x1 & 1u);
+    const uint32_t lh = (uint32_t)lane & 1u;
     uint32_t wm[NW > 0 ? NW : 1], wmr[NW > 0 ? NW : 1];
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
@@ -336,117 +352,79 @@ __global__ void __launch_bounds__(kBlockB) pms_search_block(SearchArgs a) {
         if (lane == 0) b = atomicAdd(&a.st->next, (unsigned long long)a.batch);
         b = __shfl_sync(kFull, b, 0);
         if (b >= a.span) break;
-        for (int sb = 0; sb < a.batch; sb += kSub) {
+        for (int sb = 0; sb < a.batch; sb += kBlkC) {
             const unsigned long long cbase = a.lo_al + b + sb;
             if (cbase >= a.hi) break;
             const uint32_t cb = code_to_bp((uint32_t)cbase);  // suffix bits are zero
-            uint32_t alive[kBlkWords];
-#pragma unroll
-            for (int k = 0; k < kBlkWords; ++k) alive[k] = kFull;
-            if (cbase < a.lo || cbase + kBlkC > a.hi) {  // edge block of [lo, hi)
-#pragma unroll
-                for (int k = 0; k < kBlkWords; ++k) {
-                    const unsigned long long c0 = cbase + 32u * k;
-                    uint32_t m = kFull;
-                    if (c0 < a.lo) m = (a.lo - c0 >= 32) ? 0u : m << (a.lo - c0);
-                    if (c0 + 32 > a.hi) m &= (a.hi <= c0) ? 0u : (kFull >> (c0 + 32 - a.hi));
-                    alive[k] = m;
-                }
+            const uint32_t cr = rot16(cb);
+            // this lane's 32 candidates cbase + 32*lane + [0, 32) inside [lo, hi)
+            uint32_t alive = kFull;
+            {
+                const unsigned long long c0 = cbase + 32u * lane;
+                if (c0 < a.lo) alive = (a.lo - c0 >= 32) ? 0u : alive << (a.lo - c0);
+                if (c0 + 32 > a.hi) alive &= (a.hi <= c0) ? 0u : (kFull >> (c0 + 32 - a.hi));
             }
             int i = 0;
             bool dead = false;
             for (; i < a.n; ++i) {
-                if (i > 0) {
-                    int na = 0;
-#pragma unroll
-                    for (int k = 0; k < kBlkWords; ++k) na += __popc(alive[k]);
-                    if (na <= kBlkSwitch) break;
-                }
-                uint32_t acc[kBlkWords];
-#pragma unroll
-                for (int k = 0; k < kBlkWords; ++k) acc[k] = 0u;
-                // pass 1: prefix distance of every window; hits (p2 <= d2, ~1 %
-                // of windows) are recorded in a per-lane bitmask, no branch
+                if (i > 0 && __reduce_add_sync(kFull, __popc(alive)) <= 1) break;
                 const uint32_t* row = tab + (size_t)i * a.Wp;
-                const uint32_t cr = rot16(cb);
-                if (NW > 0 && i == 0) {
+                uint32_t acc = 0;
+                // pass 1: prefix distance of each window; hits recorded per lane
+                if (NW > 0) {
                     uint32_t hm = 0;
+                    if (i == 0) {
 #pragma unroll
-                    for (int j = 0; j < NW; ++j) {
-                        const uint32_t p2 = __popc((cb ^ wm[j]) | (cr ^ wmr[j]));
-                        if (p2 <= a.d2) hm |= 1u << j;
-                    }
-                    // pass 2: the hit windows' suffix masks (window re-read from the table)
-                    while (hm) {
-                        const int j = __ffs(hm) - 1;
-                        hm &= hm - 1;
-                        const uint32_t w = row[lane + 32 * j];  // Wp == 32*NW (padded rows)
-                        const uint32_t x = (cb ^ w) & ~kSfxBits;
-                        block_hit(__popc(x | rot16(x)), w, a.d2, ball, acc);
-                    }
-                } else if (NW > 0) {  // rows hold exactly 32*NW windows
-                    uint32_t hm = 0;
+                        for (int j = 0; j < NW; ++j)
+                            if (__popc((cb ^ wm[j]) | (cr ^ wmr[j])) <= a.d2) hm |= 1u << j;
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < NW; ++j) {
-                        const uint32_t x = (cb ^ row[lane + 32 * j]) & ~kSfxBits;
-                        if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
+                        for (int j = 0; j < NW; ++j) {
+                            const uint32_t x = (cb ^ row[lane + 32 * j]) & ~kSfxBits;
+                            if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
+                        }
                     }
-                    while (hm) {
-                        const int j = __ffs(hm) - 1;
-                        hm &= hm - 1;
-                        const uint32_t w = row[lane + 32 * j];
-                        const uint32_t x = (cb ^ w) & ~kSfxBits;
-                        block_hit(__popc(x | rot16(x)), w, a.d2, ball, acc);
-                    }
+                    // pass 2: broadcast the hits; each lane ORs its own candidates
+                    drain_hits(hm, row, cb, a.d2, lane, lH01, lL01, lh, T, acc);
                 } else {
                     for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
                         uint32_t hm = 0;
-                        const int kend = min(a.Wp - k0, 32 * 32);
-#pragma unroll 4
-                        for (int j = 0; j < kend / 32; ++j) {
-                            const uint32_t w = row[k0 + lane + 32 * j];
-                            const uint32_t x = (cb ^ w) & ~kSfxBits;
-                            if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;  // 2 * prefix dist
+                        const int nj = min(a.Wp - k0, 32 * 32) / 32;
+                        for (int j = 0; j < nj; ++j) {
+                            const uint32_t x = (cb ^ row[k0 + lane + 32 * j]) & ~kSfxBits;
+                            if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
                         }
-                        while (hm) {
-                            const int j = __ffs(hm) - 1;
-                            hm &= hm - 1;
-                            const uint32_t w = row[k0 + lane + 32 * j];
-                            const uint32_t x = (cb ^ w) & ~kSfxBits;
-                            block_hit(__popc(x | rot16(x)), w, a.d2, ball, acc);
-                        }
+                        drain_hits(hm, row + k0, cb, a.d2, lane, lH01, lL01, lh, T, acc);
                     }
                 }
-                uint32_t any = 0;
-#pragma unroll
-                for (int k = 0; k < kBlkWords; ++k) {
-                    alive[k] &= __reduce_or_sync(kFull, acc[k]);
-                    any |= alive[k];
-                }
+                alive &= acc;
                 ++bscans;
-                if (!any) {  // skip rule: no block candidate matches sequence i
+                if (!__any_sync(kFull, alive != 0u)) {  // skip rule for the whole block
                     dead = true;
                     break;
                 }
             }
             if (dead) continue;
             if (i == a.n) {  // every alive candidate matched all n sequences
-#pragma unroll
-                for (int k = 0; k < kBlkWords; ++k) append_mask(a, cbase, k, alive[k], lane);
+                if (alive) {
+                    const unsigned long long slot0 = atomicAdd(a.nout, (unsigned long long)__popc(alive));
+                    uint32_t m = alive;
+                    for (unsigned long long slot = slot0; m; ++slot) {
+                        const int bit = __ffs(m) - 1;
+                        m &= m - 1;
+                        if (slot < a.cap) a.out[slot] = (uint32_t)(cbase + 32u * lane + bit);
+                    }
+                }
                 continue;
             }
-            // at most kBlkSwitch survivors: finish them one by one from sequence i on
-            uint32_t pick = 0xFFFFFFFFu;  // suffix index of the (single) survivor
-#pragma unroll
-            for (int k = kBlkWords - 1; k >= 0; --k)
-                if (alive[k]) pick = 32u * k + (__ffs(alive[k]) - 1);
-            static_assert(kBlkSwitch == 1, "survivor extraction handles one candidate");
-            if (pick != 0xFFFFFFFFu) {
-                const uint32_t code = (uint32_t)(cbase + pick);
-                if (check_sequences(tab, i, a.n, a.Wp, code_to_bp(code), a.d2, lane, scanned) &&
-                    lane == 0)
-                    append(a, code);
-            }
+            // one survivor left: the whole warp finishes it from sequence i on
+            const uint32_t holder = __ballot_sync(kFull, alive != 0u);
+            const int src = __ffs(holder) - 1;
+            const uint32_t word = __shfl_sync(kFull, alive, src);
+            const uint32_t code = (uint32_t)(cbase + 32u * src + (__ffs(word) - 1));
+            if (check_sequences(tab, i, a.n, a.Wp, code_to_bp(code), a.d2, lane, scanned) &&
+                lane == 0)
+                append(a, code);
         }
     }
     if (lane == 0) {
@@ -602,7 +580,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         destroy_plan(p);
         return PMS_E_CUDA;
     }
-    const bool block_algo = p->launch.algo == PMS_ALGO_BLOCK && !p->launch.no_skip && l > kBlkS;
+    const bool block_algo = p->launch.algo == PMS_ALGO_BLOCK && !p->launch.no_skip && l >= kBlkS;
     const BlockKernel* bk = &kBlockKernels[0];
     if (block_algo && !p->launch.force_generic)
         for (const BlockKernel& k : kBlockKernels)  // sequence 0 register-resident
@@ -613,7 +591,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
             }
     p->tab_bytes = (uint32_t)((size_t)n * p->Wp * 4);
     const uint32_t static_smem = 64;  // mbarrier + slack
-    const uint32_t ball_bytes = block_algo ? (uint32_t)kBallWords * 4u : 0u;
+    const uint32_t ball_bytes = block_algo ? 512u * 4u : 0u;  // suffix table slot
     p->in_smem = p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
     p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0);
 
@@ -687,16 +665,16 @@ extern "C" int pms_plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo,
     if (hi > total) hi = total;
     if (lo > hi) return PMS_E_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const unsigned long long lo_al = lo / kSub * kSub;
+    const unsigned long long lo_al = lo / kUnit * kUnit;
     const unsigned long long span = hi - lo_al;
 
     // batch: aim for >= 8 grabs per warp, multiple of kSub, at most 16 sub-blocks
     const unsigned long long warps = (unsigned long long)p->grid * (p->block / 32);
-    int batch = p->launch.batch > 0 ? (p->launch.batch + kSub - 1) / kSub * kSub : 0;
+    int batch = p->launch.batch > 0 ? (p->launch.batch + kUnit - 1) / kUnit * kUnit : 0;
     if (batch == 0) {
         unsigned long long b = span / (warps * 8);
-        b = (b + kSub - 1) / kSub * kSub;
-        batch = (int)std::min<unsigned long long>(std::max<unsigned long long>(b, kSub), 16 * kSub);
+        b = (b + kUnit - 1) / kUnit * kUnit;
+        batch = (int)std::min<unsigned long long>(std::max<unsigned long long>(b, kUnit), 4 * kUnit);
     }
     p->batch = batch;
     p->last_lo = lo;

@@ -282,6 +282,11 @@ def test_block_algo_tiny_random(orc):
         s = fmgen.random_sequences(n, t, 7000 + trial)
         got, _ = assert_same(s, l, d, orc, launch=BLOCK)
         assert got.stats.algo == (pms.ALGO_BLOCK if l >= 5 else pms.ALGO_CANDIDATE)
+    # 1024-candidate blocks: l = 5 is a single block with an empty prefix
+    for seed in range(5):
+        s = fmgen.random_sequences(3, 30, 60 + seed)
+        for d in range(0, 6):
+            assert_same(s, 5, d, orc, launch=BLOCK)
 
 
 def test_block_algo_planted_and_edges(orc):
@@ -303,7 +308,7 @@ def test_block_algo_ranges(orc):
     full = gpu(s, 7, 1, launch=BLOCK).codes.tolist()
     assert full == orc.find(s, 7, 1).codes.tolist()
     for lo, hi in [(0, 1), (1, 255), (3, 9), (255, 257), (300, 5000), (4095, 4 ** 7),
-                   (16383, 16384), (100, 100)]:
+                   (16383, 16384), (100, 100), (1023, 1025), (1000, 3100), (31, 33)]:
         assert_same(s, 7, 1, orc, lo=lo, hi=hi, launch=BLOCK)
     for cut in (1, 777, 8192):
         a = gpu(s, 7, 1, lo=0, hi=cut, launch=BLOCK).codes.tolist()
