@@ -247,21 +247,24 @@ constexpr int kBlkC = 1 << (2 * kBlkS);     // 1024 candidates per block
 constexpr uint32_t kSfxBits = 0x001F001Fu;  // suffix positions in both planes
 constexpr int kUnit = kBlkC;                // batch / lo alignment (multiple of kSub)
 static_assert(kUnit % kSub == 0, "batches hold whole 256-candidate sub-blocks");
-// T[r'][h][eH3][eL3] bit b: the suffix digits 2..4 of candidate x = 32L + b
-// (digit 2 = (h, b>>4) with h = L & 1, digit 3 = (b>>2)&3, digit 4 = b&3) are
-// within Hamming distance r' of the window digits 2..4 given as 3-bit planes.
-constexpr int kTR = 3;                      // r' in 0..2 tabulated; r' >= 3: all
-constexpr int kTWords = kTR * 2 * 8 * 8;    // 384 words
+// T[r'+2][h][e234] bit b, for r' in [-2, 7]: the suffix digits 2..4 of
+// candidate x = 32L + b (digit 2 = (h, b>>4) with h = L & 1, digit 3 = (b>>2)&3,
+// digit 4 = b&3) lie within Hamming distance r' of the window digits 2..4,
+// e234 = (H3 << 3) | L3 as 3-bit planes.  Rows r' < 0 are empty and rows
+// r' >= 3 are full, so a lane indexes the row r - k without clamping.
+constexpr int kTRows = 10;                        // r' + 2 in [0, 10)
+constexpr int kTWords = kTRows * 2 * 64;          // 1280 words (5 KB)
 
 __device__ __forceinline__ void build_suffix_table(uint32_t* T) {
     for (int idx = threadIdx.x; idx < kTWords; idx += blockDim.x) {
-        const uint32_t eL = idx & 7, eH = (idx >> 3) & 7, h = (idx >> 6) & 1;
-        const int r = idx >> 7;
+        const uint32_t e = idx & 63, h = (idx >> 6) & 1;
+        const int r = (idx >> 7) - 2;
+        const uint32_t eH = e >> 3, eL = e & 7;
         uint32_t word = 0;
         for (uint32_t b = 0; b < 32; ++b) {
             const uint32_t xH = (h << 2) | (((b >> 3) & 1) << 1) | ((b >> 1) & 1);
             const uint32_t xL = ((b >> 4) << 2) | (((b >> 2) & 1) << 1) | (b & 1);
-            if (__popc((xH ^ eH) | (xL ^ eL)) <= r) word |= 1u << b;
+            if ((int)__popc((xH ^ eH) | (xL ^ eL)) <= r) word |= 1u << b;
         }
         T[idx] = word;
     }
@@ -269,29 +272,28 @@ __device__ __forceinline__ void build_suffix_table(uint32_t* T) {
 
 constexpr int kBlockB = 512;  // max threads per CTA of the block kernel
 
-// Hit record of a lane: r = min(d - p, 7) budget left for the suffix, and the
-// window's 5 suffix digits as planes: v = r << 10 | H5 << 5 | L5.
+// Hit record made by the lane that found the window: v = e01 << 12 |
+// (r + 2) << 7 | e234, with r = min(d - p, 7) the suffix budget, e01 the
+// window's suffix digits 0,1 and e234 digits 2..4 (plane-packed).
 __device__ __forceinline__ uint32_t hit_record(uint32_t cb, uint32_t w, uint32_t d2) {
     const uint32_t x = (cb ^ w) & ~kSfxBits;
     const uint32_t r = min((d2 - __popc(x | rot16(x))) >> 1, 7u);
-    return (r << 10) | (((w >> 16) & 31u) << 5) | (w & 31u);
+    const uint32_t eH = (w >> 16) & 31u, eL = w & 31u;
+    return ((((eH >> 3) << 2) | (eL >> 3)) << 12) | ((r + 2) << 7) | ((eH & 7u) << 3) | (eL & 7u);
 }
 
-// Lane-side application of a broadcast hit record to this lane's word.
-__device__ __forceinline__ uint32_t hit_word(uint32_t v, uint32_t lH01, uint32_t lL01, uint32_t lh,
-                                             const uint32_t* T) {
-    const int r = (int)(v >> 10);
-    const uint32_t eH = (v >> 5) & 31u, eL = v & 31u;
-    const int rr = r - __popc(((eH >> 3) ^ lH01) | ((eL >> 3) ^ lL01));  // digits 0,1
-    const uint32_t t = T[(min(max(rr, 0), kTR - 1) << 7) | (lh << 6) | ((eH & 7u) << 3) | (eL & 7u)];
-    return rr < 0 ? 0u : (rr >= kTR ? kFull : t);
+// Lane side: kTab holds, 2 bits per e01, the number of digit-0/1 mismatches
+// between e01 and this lane's candidates; Tl = T + 64 * (lane & 1).
+__device__ __forceinline__ uint32_t hit_word(uint32_t v, uint32_t kTab, const uint32_t* Tl) {
+    const uint32_t k = (kTab >> ((v >> 11) & 30u)) & 3u;  // 2 * e01 = (v >> 11) & 30
+    return Tl[(v & 0xFFFu) - (k << 7)];
 }
 
 // Broadcast every pending hit of every lane (hm bits index the lane's windows
 // row[lane + 32*j]) and OR the matching candidates into each lane's acc.
 __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uint32_t cb,
-                                           uint32_t d2, int lane, uint32_t lH01, uint32_t lL01,
-                                           uint32_t lh, const uint32_t* T, uint32_t& acc) {
+                                           uint32_t d2, int lane, uint32_t kTab,
+                                           const uint32_t* Tl, uint32_t& acc) {
     for (;;) {
         uint32_t mine = kFull;
         if (hm) {
@@ -304,7 +306,7 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uin
         do {
             const int src = __ffs(who) - 1;
             who &= who - 1;
-            acc |= hit_word(__shfl_sync(kFull, mine, src), lH01, lL01, lh, T);
+            acc |= hit_word(__shfl_sync(kFull, mine, src), kTab, Tl);
         } while (who);
     }
 }
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
     __shared__ __align__(8) uint64_t bar;
     if (*(volatile unsigned int*)&a.st->bad) return;
     uint32_t* T = stab;
-    uint32_t* tsm = stab + 512;  // keeps the table 2 KB-aligned for the bulk copy
+    uint32_t* tsm = stab + kTWords;  // 5 KB: keeps the table 128-B aligned for the bulk copy
     if (SMEM) {  // start the table's TMA bulk copy, build the suffix table meanwhile
         if (threadIdx.x == 0) mbar_init(&bar, 1);
         __syncthreads();
@@ -335,10 +337,15 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
     if (SMEM) mbar_wait(&bar, 0);
     const uint32_t* tab = SMEM ? tsm : a.tab;
     const int lane = threadIdx.x & 31;
-    // this lane's candidate digits 0,1 (planes) and the high bit of digit 2
+    // this lane's candidates: digits 0,1 = (lane >> 3, (lane >> 1) & 3) and the
+    // high bit of digit 2 = lane & 1.  kTab: digit-0/1 mismatches per window e01.
     const uint32_t x0 = (uint32_t)lane >> 3, x1 = ((uint32_t)lane >> 1) & 3u;
     const uint32_t lH01 = ((x0 >> 1) << 1) | (x1 >> 1), lL01 = ((x0 & 1u) << 1) | (x1 & 1u);
-    const uint32_t lh = (uint32_t)lane & 1u;
+    uint32_t kTab = 0;
+#pragma unroll
+    for (uint32_t e01 = 0; e01 < 16; ++e01)
+        kTab |= (uint32_t)__popc(((e01 >> 2) ^ lH01) | ((e01 & 3u) ^ lL01)) << (2 * e01);
+    const uint32_t* Tl = T + 64 * (lane & 1);
     uint32_t wm[NW > 0 ? NW : 1], wmr[NW > 0 ? NW : 1];
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
                         }
                     }
                     // pass 2: broadcast the hits; each lane ORs its own candidates
-                    drain_hits(hm, row, cb, a.d2, lane, lH01, lL01, lh, T, acc);
+                    drain_hits(hm, row, cb, a.d2, lane, kTab, Tl, acc);
                 } else {
                     for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
                         uint32_t hm = 0;
@@ -394,7 +401,7 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
                             const uint32_t x = (cb ^ row[k0 + lane + 32 * j]) & ~kSfxBits;
                             if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
                         }
-                        drain_hits(hm, row + k0, cb, a.d2, lane, lH01, lL01, lh, T, acc);
+                        drain_hits(hm, row + k0, cb, a.d2, lane, kTab, Tl, acc);
                     }
                 }
                 alive &= acc;
@@ -591,7 +598,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
             }
     p->tab_bytes = (uint32_t)((size_t)n * p->Wp * 4);
     const uint32_t static_smem = 64;  // mbarrier + slack
-    const uint32_t ball_bytes = block_algo ? 512u * 4u : 0u;  // suffix table slot
+    const uint32_t ball_bytes = block_algo ? (uint32_t)kTWords * 4u : 0u;  // suffix table
     p->in_smem = p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
     p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0);
 
