@@ -289,26 +289,41 @@ __device__ __forceinline__ uint32_t hit_word(uint32_t v, uint32_t kTab, const ui
     return Tl[(v & 0xFFFu) - (k << 7)];
 }
 
-// Broadcast every pending hit of every lane (hm bits index the lane's windows
-// row[lane + 32*j]) and OR the matching candidates into each lane's acc.
+// Process every pending hit of every lane (hm bits index the lane's windows
+// row[lane + 32*j]) and OR the matching candidates into each lane's acc.  A
+// hit with no suffix budget left (p == d, ~80 % of hits) matches exactly one
+// candidate -- the window's own suffix -- so the finding lane sets that bit in
+// the warp's shared-memory mask with one atomic OR; hits with budget >= 1 are
+// broadcast (one SHFL) and every lane ORs its word from the suffix table.
 __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uint32_t cb,
                                            uint32_t d2, int lane, uint32_t kTab,
-                                           const uint32_t* Tl, uint32_t& acc) {
-    for (;;) {
+                                           const uint32_t* Tl, uint32_t* wmask, uint32_t& acc) {
+    while (__any_sync(kFull, hm != 0u)) {
         uint32_t mine = kFull;
         if (hm) {
             const int j = __ffs(hm) - 1;
             hm &= hm - 1;
-            mine = hit_record(cb, row[lane + 32 * j], d2);
+            const uint32_t w = row[lane + 32 * j];
+            const uint32_t x = (cb ^ w) & ~kSfxBits;
+            const uint32_t p2 = __popc(x | rot16(x));
+            if (p2 == d2) {
+                const uint32_t sx = (spread_even((w >> 16) & 31u) << 1) | spread_even(w & 31u);
+                atomicOr(&wmask[sx >> 5], 1u << (sx & 31u));
+            } else {
+                mine = hit_record(cb, w, d2);
+            }
         }
         uint32_t who = __ballot_sync(kFull, mine != kFull);
-        if (!who) break;
-        do {
+        while (who) {
             const int src = __ffs(who) - 1;
             who &= who - 1;
             acc |= hit_word(__shfl_sync(kFull, mine, src), kTab, Tl);
-        } while (who);
+        }
     }
+    __syncwarp();
+    acc |= wmask[lane];
+    wmask[lane] = 0u;
+    __syncwarp();
 }
 
 // NW > 0: lane keeps windows lane + 32j (j < NW) of sequence 0 in registers,
@@ -317,8 +332,11 @@ template <bool SMEM, int NW>
 __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(SearchArgs a) {
     extern __shared__ __align__(128) uint32_t stab[];  // [T][table if SMEM]
     __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t wmasks[kBlockB / 32][32];  // per-warp single-candidate hit masks
     if (*(volatile unsigned int*)&a.st->bad) return;
     uint32_t* T = stab;
+    uint32_t* wmask = wmasks[threadIdx.x >> 5];
+    wmask[threadIdx.x & 31] = 0u;
     uint32_t* tsm = stab + kTWords;  // 5 KB: keeps the table 128-B aligned for the bulk copy
     if (SMEM) {  // start the table's TMA bulk copy, build the suffix table meanwhile
         if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -392,7 +410,7 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
                         }
                     }
                     // pass 2: broadcast the hits; each lane ORs its own candidates
-                    drain_hits(hm, row, cb, a.d2, lane, kTab, Tl, acc);
+                    drain_hits(hm, row, cb, a.d2, lane, kTab, Tl, wmask, acc);
                 } else {
                     for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
                         uint32_t hm = 0;
@@ -401,7 +419,7 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
                             const uint32_t x = (cb ^ row[k0 + lane + 32 * j]) & ~kSfxBits;
                             if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
                         }
-                        drain_hits(hm, row + k0, cb, a.d2, lane, kTab, Tl, acc);
+                        drain_hits(hm, row + k0, cb, a.d2, lane, kTab, Tl, wmask, acc);
                     }
                 }
                 alive &= acc;
@@ -597,7 +615,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
                 break;
             }
     p->tab_bytes = (uint32_t)((size_t)n * p->Wp * 4);
-    const uint32_t static_smem = 64;  // mbarrier + slack
+    const uint32_t static_smem = 4096;  // mbarrier, per-warp hit masks, slack
     const uint32_t ball_bytes = block_algo ? (uint32_t)kTWords * 4u : 0u;  // suffix table
     p->in_smem = p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
     p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0);
