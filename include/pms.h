@@ -71,14 +71,16 @@ typedef struct pms_launch {
 /* Kernel families (pms_launch.algo).  Every family returns the same set.
  *   PMS_ALGO_CANDIDATE: one candidate per 16/32 lanes; each candidate-window
  *     Hamming test is XOR, XOR-OR fold, POPC.
- *   PMS_ALGO_BLOCK: the 256 candidates that share their first l-4 digits are
- *     tested together: one XOR/fold/POPC of the shared prefix against a window
- *     gives the prefix distance p, and the candidates whose last 4 digits lie
- *     within d-p of the window's last 4 digits (a precomputed Hamming-ball
- *     bitmask) match that window.  The skip rule applies to the block's alive
- *     mask: the block is abandoned at the first sequence where no alive
- *     candidate matches; few survivors fall back to per-candidate checks.
- *     Needs l >= 5 (else the candidate family runs). */
+ *   PMS_ALGO_BLOCK: the 1024 candidates sharing their first l-5 digits are
+ *     tested together (bit-parallel over candidates): one XOR/fold/POPC of the
+ *     shared prefix against a window gives the prefix distance p, and the
+ *     candidates whose last 5 digits lie within d-p of the window's last 5
+ *     digits match that window (a Hamming-ball bitmask).  Each candidate keeps
+ *     PAPER.md:63's semantics: it is compared with the windows of sequence
+ *     0, 1, ... and dropped at the first sequence with no window within d; the
+ *     block is abandoned when no candidate is left (the skip rule on 1024
+ *     candidates at once).  Needs l >= 5 (else the candidate family runs).
+ *   PMS_ALGO_AUTO (0): PMS_ALGO_BLOCK when l >= 5, else PMS_ALGO_CANDIDATE. */
 enum { PMS_ALGO_AUTO = 0, PMS_ALGO_CANDIDATE = 1, PMS_ALGO_BLOCK = 2 };
 
 /* Counters and timings of the last execution of a plan. */

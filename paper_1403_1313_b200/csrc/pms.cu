@@ -605,7 +605,8 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         destroy_plan(p);
         return PMS_E_CUDA;
     }
-    const bool block_algo = p->launch.algo == PMS_ALGO_BLOCK && !p->launch.no_skip && l >= kBlkS;
+    const bool block_algo = (p->launch.algo == PMS_ALGO_BLOCK || p->launch.algo == PMS_ALGO_AUTO) &&
+                            !p->launch.no_skip && l >= kBlkS;
     const BlockKernel* bk = &kBlockKernels[0];
     if (block_algo && !p->launch.force_generic)
         for (const BlockKernel& k : kBlockKernels)  // sequence 0 register-resident

@@ -31,6 +31,9 @@ def _gpu():
     pms.load()
 
 
+CAND = pms.Launch(algo=pms.ALGO_CANDIDATE)
+
+
 def gpu(seqs, l, d, **kw):
     r = pms.find_ex(seqs, l, d, max_out=kw.pop("max_out", 1 << 22), **kw)
     return r
@@ -55,7 +58,9 @@ def test_tiny_random_instances(orc):
         t = rng.randint(l, 70)
         d = rng.randint(0, min(3, l))
         s = fmgen.random_sequences(n, t, 500 + trial)
-        assert_same(s, l, d, orc)
+        got, _ = assert_same(s, l, d, orc)  # default family (AUTO)
+        assert got.stats.algo == (pms.ALGO_BLOCK if l >= 5 else pms.ALGO_CANDIDATE)
+        assert_same(s, l, d, orc, launch=CAND)
 
 
 def test_planted_small_configs(orc):
@@ -75,7 +80,7 @@ def test_window_counts_and_padding(orc, W):
     t = W + l - 1
     n = 3 if W < 1000 else 2
     s, _ = fmgen.generate_fm(n, t, l, d, W)
-    assert_same(s, l, d, orc)
+    assert_same(s, l, d, orc, launch=CAND)
 
 
 @pytest.mark.parametrize("l,d", [(1, 0), (1, 1), (2, 0), (2, 1), (3, 1), (4, 0), (5, 2), (8, 8),
@@ -138,13 +143,13 @@ def test_truncation_and_size_query(orc):
 
 def test_ranges_and_additivity(orc):
     s, _ = fmgen.generate_fm(5, 60, 7, 1, 4)
-    full = gpu(s, 7, 1).codes.tolist()
+    full = gpu(s, 7, 1, launch=CAND).codes.tolist()
     for lo, hi in [(0, 0), (0, 1), (1, 255), (255, 257), (300, 5000), (4095, 4 ** 7),
                    (16383, 16384)]:
-        assert_same(s, 7, 1, orc, lo=lo, hi=hi)
+        assert_same(s, 7, 1, orc, lo=lo, hi=hi, launch=CAND)
     for cut in (0, 1, 777, 8192, 16384):
-        a = gpu(s, 7, 1, lo=0, hi=cut).codes.tolist()
-        b = gpu(s, 7, 1, lo=cut, hi=4 ** 7).codes.tolist()
+        a = gpu(s, 7, 1, lo=0, hi=cut, launch=CAND).codes.tolist()
+        b = gpu(s, 7, 1, lo=cut, hi=4 ** 7, launch=CAND).codes.tolist()
         assert a + b == full
 
 
@@ -154,7 +159,7 @@ def test_launch_configuration_invariance():
     for kw in [dict(lanes_per_cand=16), dict(lanes_per_cand=32), dict(force_generic=1),
                dict(ctas_per_sm=1, warps_per_cta=1), dict(batch=256), dict(batch=4096),
                dict(warps_per_cta=3, batch=512)]:
-        L = pms.Launch(**kw)
+        L = pms.Launch(algo=pms.ALGO_CANDIDATE, **kw)
         for _ in range(2):  # determinism across repeated runs
             assert gpu(s, 11, 3, launch=L).codes.tolist() == base, kw
 
@@ -162,9 +167,9 @@ def test_launch_configuration_invariance():
 def test_table_in_global_memory(orc):
     # n * Wp * 4 = 100 * 608 * 4 = 243,200 B > 227 KB opt-in smem -> global table
     s, _ = fmgen.generate_fm(100, 600, 9, 2, 5)
-    got, _ = assert_same(s, 9, 2, orc)
+    got, _ = assert_same(s, 9, 2, orc, launch=CAND)
     assert got.stats.table_in_smem == 0
-    got = gpu(s, 9, 2, launch=pms.Launch(force_generic=1))
+    got = gpu(s, 9, 2, launch=pms.Launch(algo=pms.ALGO_CANDIDATE, force_generic=1))
     assert got.codes.tolist() == orc.find(s, 9, 2).codes.tolist()
 
 
@@ -226,7 +231,7 @@ def test_baseline_configs_against_golden(orc, path):
     g = json.load(open(path))
     s, rec = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
     assert rec.consensus == g["consensus"]  # the generator reproduces the golden input
-    r = gpu(s, g["l"], g["d"])
+    r = gpu(s, g["l"], g["d"], launch=CAND)
     assert r.status == 0
     assert r.count == g["count"]
     assert r.codes.tolist() == g["codes"]
@@ -262,9 +267,10 @@ def test_naive_brute_force_variant(orc):
 def test_grid_size_override():
     s, _ = fmgen.generate_fm(20, 600, 10, 2, 3)
     base = gpu(s, 10, 2).codes.tolist()
-    for g in (1, 2, 7, 148):
-        r = gpu(s, 10, 2, launch=pms.Launch(grid_ctas=g))
-        assert r.stats.grid == g and r.codes.tolist() == base
+    for algo in (pms.ALGO_CANDIDATE, pms.ALGO_BLOCK):
+        for g in (1, 2, 7, 148):
+            r = gpu(s, 10, 2, launch=pms.Launch(grid_ctas=g, algo=algo))
+            assert r.stats.grid == g and r.codes.tolist() == base
 
 
 # ------------------------------------------------ PMS_ALGO_BLOCK family
@@ -350,6 +356,7 @@ def test_block_algo_launch_invariance():
 def test_block_algo_baseline_configs(orc, path):
     g = json.load(open(path))
     s, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
-    r = gpu(s, g["l"], g["d"], launch=BLOCK)
-    assert r.status == 0 and r.stats.algo == pms.ALGO_BLOCK
-    assert r.count == g["count"] and r.codes.tolist() == g["codes"]
+    for launch in (BLOCK, None):  # explicit and the default (AUTO) family
+        r = gpu(s, g["l"], g["d"], launch=launch)
+        assert r.status == 0 and r.stats.algo == pms.ALGO_BLOCK
+        assert r.count == g["count"] and r.codes.tolist() == g["codes"]
