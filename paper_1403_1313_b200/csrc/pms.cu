@@ -19,7 +19,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <vector>
 
 #include "pms.h"
 #include "pms_device.cuh"
@@ -778,16 +780,85 @@ extern "C" int pms_plan_wait(pms_plan* p, pms_stats* stats) {
 // ========================================================================
 namespace {
 
-struct DevBufs {
-    uint8_t* seqs = nullptr;
-    uint32_t* out = nullptr;
-    uint64_t* count = nullptr;
-    ~DevBufs() {
-        cudaFree(seqs);
-        cudaFree(out);
-        cudaFree(count);
+// A reusable host-call context: plan + device buffers + stream + pinned count.
+// pms_find/pms_find_ex keep idle contexts in a small process-wide pool keyed
+// by (device, shape, launch) so repeated calls skip allocation and setup.
+struct CallCtx {
+    int dev = 0;
+    int32_t n = 0, t = 0, l = 0, d = 0;
+    pms_launch launch{};
+    pms_plan* plan = nullptr;
+    uint8_t* d_seqs = nullptr;
+    uint32_t* d_out = nullptr;
+    unsigned long long out_cap = 0;
+    uint64_t* d_count = nullptr;
+    uint64_t* h_count = nullptr;  // pinned
+    cudaStream_t stream = nullptr;
+
+    bool matches(int dv, int32_t n_, int32_t t_, int32_t l_, int32_t d_,
+                 const pms_launch& L) const {
+        return dev == dv && n == n_ && t == t_ && l == l_ && d == d_ &&
+               std::memcmp(&launch, &L, sizeof(L)) == 0;
+    }
+    void release_resources() {
+        destroy_plan(plan);
+        cudaFree(d_seqs);
+        cudaFree(d_out);
+        cudaFree(d_count);
+        cudaFreeHost(h_count);
+        if (stream) cudaStreamDestroy(stream);
     }
 };
+
+std::mutex g_pool_mu;
+std::vector<CallCtx*> g_pool;
+constexpr size_t kPoolMax = 8;
+
+void ctx_destroy(CallCtx* c) {
+    if (!c) return;
+    c->release_resources();
+    delete c;
+}
+
+int ctx_acquire(int32_t n, int32_t t, int32_t l, int32_t d, const pms_launch& L, CallCtx** out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return PMS_E_CUDA;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (size_t i = 0; i < g_pool.size(); ++i)
+            if (g_pool[i]->matches(dev, n, t, l, d, L)) {
+                *out = g_pool[i];
+                g_pool.erase(g_pool.begin() + (long)i);
+                return PMS_OK;
+            }
+    }
+    CallCtx* c = new (std::nothrow) CallCtx();
+    if (!c) return PMS_E_CUDA;
+    c->dev = dev; c->n = n; c->t = t; c->l = l; c->d = d; c->launch = L;
+    int st = pms_plan_create(n, t, l, d, &L, &c->plan);
+    if (st != PMS_OK) {
+        delete c;
+        return st;
+    }
+    if (cudaMalloc(&c->d_seqs, (size_t)n * t) != cudaSuccess ||
+        cudaMalloc(&c->d_count, sizeof(uint64_t)) != cudaSuccess ||
+        cudaMallocHost(&c->h_count, sizeof(uint64_t)) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        ctx_destroy(c);
+        return PMS_E_CUDA;
+    }
+    *out = c;
+    return PMS_OK;
+}
+
+void ctx_release(CallCtx* c) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (g_pool.size() < kPoolMax) {
+        g_pool.push_back(c);
+        return;
+    }
+    ctx_destroy(c);
+}
 
 }  // namespace
 
@@ -803,47 +874,65 @@ extern "C" int pms_find_ex(const uint8_t* seqs, int32_t n, int32_t t, int32_t l,
     if (lo > hi) return PMS_E_ARG;
     *count = 0;
 
-    pms_plan* plan = nullptr;
-    st = pms_plan_create(n, t, l, d, launch, &plan);
+    const pms_launch L = launch ? *launch : pms_launch{};
+    CallCtx* c = nullptr;
+    st = ctx_acquire(n, t, l, d, L, &c);
     if (st != PMS_OK) return st;
-    struct PlanGuard {
-        pms_plan* p;
-        ~PlanGuard() { destroy_plan(p); }
-    } guard{plan};
+    bool healthy = true;
+    struct Guard {
+        CallCtx* c;
+        bool* healthy;
+        ~Guard() {
+            if (*healthy) ctx_release(c);
+            else ctx_destroy(c);
+        }
+    } guard{c, &healthy};
 
     const unsigned long long cap = std::min<unsigned long long>(max_out, hi - lo);
-    DevBufs b;
-    const size_t nbytes = (size_t)n * t;
-    if (cudaMalloc(&b.seqs, nbytes) != cudaSuccess ||
-        cudaMalloc(&b.count, sizeof(uint64_t)) != cudaSuccess ||
-        (cap > 0 && cudaMalloc(&b.out, cap * sizeof(uint32_t)) != cudaSuccess))
+    if (cap > c->out_cap) {  // grow the result buffer (kept for the next call)
+        cudaFree(c->d_out);
+        c->d_out = nullptr;
+        c->out_cap = 0;
+        if (cudaMalloc(&c->d_out, cap * sizeof(uint32_t)) != cudaSuccess) {
+            healthy = false;
+            return PMS_E_CUDA;
+        }
+        c->out_cap = cap;
+    }
+    cudaStream_t s = c->stream;
+    if (cudaMemcpyAsync(c->d_seqs, seqs, (size_t)n * t, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        healthy = false;
         return PMS_E_CUDA;
-    cudaStream_t s = nullptr;
-    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return PMS_E_CUDA;
-    struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } sguard{s};
-
-    if (cudaMemcpyAsync(b.seqs, seqs, nbytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    }
+    st = pms_plan_execute(c->plan, c->d_seqs, lo, hi, c->d_out, cap, c->d_count, s);
+    if (st != PMS_OK) {
+        healthy = false;
+        return st;
+    }
+    if (cudaMemcpyAsync(c->h_count, c->d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
+        cudaSuccess) {
+        healthy = false;
         return PMS_E_CUDA;
-    st = pms_plan_execute(plan, b.seqs, lo, hi, b.out, cap, b.count, s);
+    }
+    st = pms_plan_wait(c->plan, stats);
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+        healthy = false;
+        return PMS_E_CUDA;
+    }
+    if (st == PMS_E_CUDA) healthy = false;
     if (st != PMS_OK) return st;
-    uint64_t found = 0;
-    if (cudaMemcpyAsync(&found, b.count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
-        cudaSuccess)
-        return PMS_E_CUDA;
-    st = pms_plan_wait(plan, stats);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return PMS_E_CUDA;
-    if (st != PMS_OK) return st;
+    const uint64_t found = *c->h_count;
     if (stats) stats->motifs = found;
     *count = found;
     if (found > max_out) return PMS_E_TRUNCATED;
     // a7: D2H of the codes, host sort (ascending code = lexicographic order)
     if (found > 0) {
-        if (cudaMemcpy(out_codes, b.out, found * sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
-            cudaSuccess)
+        if (cudaMemcpyAsync(out_codes, c->d_out, found * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                            s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            healthy = false;
             return PMS_E_CUDA;
+        }
         std::sort(out_codes, out_codes + found);
     }
     return PMS_OK;

@@ -360,3 +360,30 @@ def test_block_algo_baseline_configs(orc, path):
         r = gpu(s, g["l"], g["d"], launch=launch)
         assert r.status == 0 and r.stats.algo == pms.ALGO_BLOCK
         assert r.count == g["count"] and r.codes.tolist() == g["codes"]
+
+
+def test_concurrent_host_calls_and_context_reuse(orc):
+    """pms_find_ex from several host threads at once (ctypes drops the GIL):
+    each call takes its own pooled context; results stay exact."""
+    import threading
+    inputs = [fmgen.generate_fm(8, 150, 8, 2, 300 + k)[0] for k in range(6)]
+    want = [orc.find(s, 8, 2).codes.tolist() for s in inputs]
+    got = [None] * len(inputs)
+
+    def work(k):
+        for _ in range(3):
+            got[k] = gpu(inputs[k], 8, 2).codes.tolist()
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(len(inputs))]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert got == want
+    # a pooled context must not leak state between shapes / ranges / bad inputs
+    bad = inputs[0].copy()
+    bad[1, 1] = ord("N")
+    assert gpu(bad, 8, 2).status == pms.E_CHAR
+    assert gpu(inputs[0], 8, 2).codes.tolist() == want[0]
+    assert gpu(inputs[0], 8, 2, lo=5000, hi=9000).codes.tolist() == \
+        orc.find(inputs[0], 8, 2, lo=5000, hi=9000).codes.tolist()
