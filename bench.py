@@ -369,7 +369,7 @@ def run_gpu(args) -> int:
         "e2e": {"value": world * args.e2e_steps * total / (e2e_tot * 1e-3),
                 "unit": "candidates/s", "h2d_bytes_per_step": n * t,
                 "d2h_bytes_per_step": 8 + 4 * nfound + 32,
-                "path": "pms_find_ex from host buffers (plan create, H2D, kernels, D2H, sort)"},
+                "path": "pms_find_ex from host buffers (pooled context, H2D, kernels, D2H, sort)"},
         "gpu_launches": 2 * args.steps,
         "clocks": cs,
     }
