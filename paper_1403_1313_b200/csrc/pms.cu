@@ -249,57 +249,46 @@ constexpr int kBlkC = 1 << (2 * kBlkS);     // 1024 candidates per block
 constexpr uint32_t kSfxBits = 0x001F001Fu;  // suffix positions in both planes
 constexpr int kUnit = kBlkC;                // batch / lo alignment (multiple of kSub)
 static_assert(kUnit % kSub == 0, "batches hold whole 256-candidate sub-blocks");
-// T[r'+2][h][e234] bit b, for r' in [-2, 7]: the suffix digits 2..4 of
-// candidate x = 32L + b (digit 2 = (h, b>>4) with h = L & 1, digit 3 = (b>>2)&3,
-// digit 4 = b&3) lie within Hamming distance r' of the window digits 2..4,
-// e234 = (H3 << 3) | L3 as 3-bit planes.  Rows r' < 0 are empty and rows
-// r' >= 3 are full, so a lane indexes the row r - k without clamping.
-constexpr int kTRows = 10;                        // r' + 2 in [0, 10)
-constexpr int kTWords = kTRows * 2 * 64;          // 1280 words (5 KB)
+// Candidates of a block are indexed in BIT-PLANE order: the block candidate
+// with suffix planes (H5, L5) -- H5 = high bits, L5 = low bits of its last 5
+// base codes, position l-5 in bit 4 -- is owned by lane H5, bit L5.  Its
+// distance to a window suffix (eH, eL) is popc((H5 ^ eH) | (L5 ^ eL)).
+// T[r][mh][eL] bit b (r in 0..5, r = 5 meaning every suffix): popc(mh | (b ^ eL))
+// <= r, i.e. lane L's candidates within r of the window when mh = L ^ eH.
+constexpr int kTR = 6;                            // r in [0, 5]
+constexpr int kTWords = kTR * 32 * 32;            // 6144 words (24 KB)
 
 __device__ __forceinline__ void build_suffix_table(uint32_t* T) {
     for (int idx = threadIdx.x; idx < kTWords; idx += blockDim.x) {
-        const uint32_t e = idx & 63, h = (idx >> 6) & 1;
-        const int r = (idx >> 7) - 2;
-        const uint32_t eH = e >> 3, eL = e & 7;
+        const uint32_t eL = idx & 31, mh = (idx >> 5) & 31;
+        const int r = idx >> 10;
         uint32_t word = 0;
-        for (uint32_t b = 0; b < 32; ++b) {
-            const uint32_t xH = (h << 2) | (((b >> 3) & 1) << 1) | ((b >> 1) & 1);
-            const uint32_t xL = ((b >> 4) << 2) | (((b >> 2) & 1) << 1) | (b & 1);
-            if ((int)__popc((xH ^ eH) | (xL ^ eL)) <= r) word |= 1u << b;
-        }
+        for (uint32_t b = 0; b < 32; ++b)
+            if ((int)__popc(mh | (b ^ eL)) <= r) word |= 1u << b;
         T[idx] = word;
     }
 }
 
 constexpr int kBlockB = 512;  // max threads per CTA of the block kernel
 
-// Hit record made by the lane that found the window: v = e01 << 12 |
-// (r + 2) << 7 | e234, with r = min(d - p, 7) the suffix budget, e01 the
-// window's suffix digits 0,1 and e234 digits 2..4 (plane-packed).
-__device__ __forceinline__ uint32_t hit_record(uint32_t cb, uint32_t w, uint32_t d2) {
-    const uint32_t x = (cb ^ w) & ~kSfxBits;
-    const uint32_t r = min((d2 - __popc(x | rot16(x))) >> 1, 7u);
-    const uint32_t eH = (w >> 16) & 31u, eL = w & 31u;
-    return ((((eH >> 3) << 2) | (eL >> 3)) << 12) | ((r + 2) << 7) | ((eH & 7u) << 3) | (eL & 7u);
-}
-
-// Lane side: kTab holds, 2 bits per e01, the number of digit-0/1 mismatches
-// between e01 and this lane's candidates; Tl = T + 64 * (lane & 1).
-__device__ __forceinline__ uint32_t hit_word(uint32_t v, uint32_t kTab, const uint32_t* Tl) {
-    const uint32_t k = (kTab >> ((v >> 11) & 30u)) & 3u;  // 2 * e01 = (v >> 11) & 30
-    return Tl[(v & 0xFFFu) - (k << 7)];
+// Hit record made by the lane that found the window: v = r << 10 | eH << 5 |
+// eL with r = min(d - p, 5) the suffix budget and (eH, eL) the window suffix
+// planes.  Lane L's table index is then v ^ (L << 5): row r, mh = eH ^ L, eL.
+__device__ __forceinline__ uint32_t hit_record(uint32_t w, uint32_t p2, uint32_t d2) {
+    const uint32_t r = min((d2 - p2) >> 1, 5u);
+    return (r << 10) | (((w >> 16) & 31u) << 5) | (w & 31u);
 }
 
 // Process every pending hit of every lane (hm bits index the lane's windows
 // row[lane + 32*j]) and OR the matching candidates into each lane's acc.  A
 // hit with no suffix budget left (p == d, ~80 % of hits) matches exactly one
-// candidate -- the window's own suffix -- so the finding lane sets that bit in
-// the warp's shared-memory mask with one atomic OR; hits with budget >= 1 are
-// broadcast (one SHFL) and every lane ORs its word from the suffix table.
+// candidate -- the window's own suffix, lane eH bit eL -- which the finding
+// lane sets in the warp's shared-memory mask with one atomic OR; hits with
+// budget >= 1 are broadcast (one SHFL) and every lane ORs T[v ^ (lane << 5)].
 __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uint32_t cb,
-                                           uint32_t d2, int lane, uint32_t kTab,
-                                           const uint32_t* Tl, uint32_t* wmask, uint32_t& acc) {
+                                           uint32_t d2, int lane, const uint32_t* T,
+                                           uint32_t* wmask, uint32_t& acc) {
+    const uint32_t lane5 = (uint32_t)lane << 5;
     while (__any_sync(kFull, hm != 0u)) {
         uint32_t mine = kFull;
         if (hm) {
@@ -308,24 +297,27 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uin
             const uint32_t w = row[lane + 32 * j];
             const uint32_t x = (cb ^ w) & ~kSfxBits;
             const uint32_t p2 = __popc(x | rot16(x));
-            if (p2 == d2) {
-                const uint32_t sx = (spread_even((w >> 16) & 31u) << 1) | spread_even(w & 31u);
-                atomicOr(&wmask[sx >> 5], 1u << (sx & 31u));
-            } else {
-                mine = hit_record(cb, w, d2);
-            }
+            if (p2 == d2)
+                atomicOr(&wmask[(w >> 16) & 31u], 1u << (w & 31u));
+            else
+                mine = hit_record(w, p2, d2);
         }
         uint32_t who = __ballot_sync(kFull, mine != kFull);
         while (who) {
             const int src = __ffs(who) - 1;
             who &= who - 1;
-            acc |= hit_word(__shfl_sync(kFull, mine, src), kTab, Tl);
+            acc |= T[__shfl_sync(kFull, mine, src) ^ lane5];
         }
     }
     __syncwarp();
     acc |= wmask[lane];
     wmask[lane] = 0u;
     __syncwarp();
+}
+
+// Suffix code (5 digits, big-endian base 4) of block candidate (H5 = lane, L5 = bit).
+__device__ __forceinline__ uint32_t sfx_code(uint32_t h5, uint32_t l5) {
+    return (spread_even(h5) << 1) | spread_even(l5);
 }
 
 // NW > 0: lane keeps windows lane + 32j (j < NW) of sequence 0 in registers,
@@ -357,15 +349,6 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
     if (SMEM) mbar_wait(&bar, 0);
     const uint32_t* tab = SMEM ? tsm : a.tab;
     const int lane = threadIdx.x & 31;
-    // this lane's candidates: digits 0,1 = (lane >> 3, (lane >> 1) & 3) and the
-    // high bit of digit 2 = lane & 1.  kTab: digit-0/1 mismatches per window e01.
-    const uint32_t x0 = (uint32_t)lane >> 3, x1 = ((uint32_t)lane >> 1) & 3u;
-    const uint32_t lH01 = ((x0 >> 1) << 1) | (x1 >> 1), lL01 = ((x0 & 1u) << 1) | (x1 & 1u);
-    uint32_t kTab = 0;
-#pragma unroll
-    for (uint32_t e01 = 0; e01 < 16; ++e01)
-        kTab |= (uint32_t)__popc(((e01 >> 2) ^ lH01) | ((e01 & 3u) ^ lL01)) << (2 * e01);
-    const uint32_t* Tl = T + 64 * (lane & 1);
     uint32_t wm[NW > 0 ? NW : 1], wmr[NW > 0 ? NW : 1];
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
@@ -384,12 +367,14 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
             if (cbase >= a.hi) break;
             const uint32_t cb = code_to_bp((uint32_t)cbase);  // suffix bits are zero
             const uint32_t cr = rot16(cb);
-            // this lane's 32 candidates cbase + 32*lane + [0, 32) inside [lo, hi)
+            // this lane's 32 candidates (H5 = lane, L5 = bit) inside [lo, hi)
             uint32_t alive = kFull;
-            {
-                const unsigned long long c0 = cbase + 32u * lane;
-                if (c0 < a.lo) alive = (a.lo - c0 >= 32) ? 0u : alive << (a.lo - c0);
-                if (c0 + 32 > a.hi) alive &= (a.hi <= c0) ? 0u : (kFull >> (c0 + 32 - a.hi));
+            if (cbase < a.lo || cbase + kBlkC > a.hi) {  // edge block of [lo, hi)
+                alive = 0u;
+                for (uint32_t bb = 0; bb < 32; ++bb) {
+                    const unsigned long long c = cbase + sfx_code((uint32_t)lane, bb);
+                    if (c >= a.lo && c < a.hi) alive |= 1u << bb;
+                }
             }
             int i = 0;
             bool dead = false;
@@ -412,7 +397,7 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
                         }
                     }
                     // pass 2: broadcast the hits; each lane ORs its own candidates
-                    drain_hits(hm, row, cb, a.d2, lane, kTab, Tl, wmask, acc);
+                    drain_hits(hm, row, cb, a.d2, lane, T, wmask, acc);
                 } else {
                     for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
                         uint32_t hm = 0;
@@ -421,7 +406,7 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
                             const uint32_t x = (cb ^ row[k0 + lane + 32 * j]) & ~kSfxBits;
                             if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
                         }
-                        drain_hits(hm, row + k0, cb, a.d2, lane, kTab, Tl, wmask, acc);
+                        drain_hits(hm, row + k0, cb, a.d2, lane, T, wmask, acc);
                     }
                 }
                 alive &= acc;
@@ -439,7 +424,7 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
                     for (unsigned long long slot = slot0; m; ++slot) {
                         const int bit = __ffs(m) - 1;
                         m &= m - 1;
-                        if (slot < a.cap) a.out[slot] = (uint32_t)(cbase + 32u * lane + bit);
+                        if (slot < a.cap) a.out[slot] = (uint32_t)(cbase + sfx_code(lane, bit));
                     }
                 }
                 continue;
@@ -448,7 +433,7 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
             const uint32_t holder = __ballot_sync(kFull, alive != 0u);
             const int src = __ffs(holder) - 1;
             const uint32_t word = __shfl_sync(kFull, alive, src);
-            const uint32_t code = (uint32_t)(cbase + 32u * src + (__ffs(word) - 1));
+            const uint32_t code = (uint32_t)(cbase + sfx_code(src, __ffs(word) - 1));
             if (check_sequences(tab, i, a.n, a.Wp, code_to_bp(code), a.d2, lane, scanned) &&
                 lane == 0)
                 append(a, code);
