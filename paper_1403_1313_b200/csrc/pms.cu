@@ -253,14 +253,16 @@ static_assert(kUnit % kSub == 0, "batches hold whole 256-candidate sub-blocks");
 // with suffix planes (H5, L5) -- H5 = high bits, L5 = low bits of its last 5
 // base codes, position l-5 in bit 4 -- is owned by lane H5, bit L5.  Its
 // distance to a window suffix (eH, eL) is popc((H5 ^ eH) | (L5 ^ eL)).
-// T[r][mh][eL] bit b (r in 0..5, r = 5 meaning every suffix): popc(mh | (b ^ eL))
-// <= r, i.e. lane L's candidates within r of the window when mh = L ^ eH.
+// T[r][eL][mh] bit b (r in 0..5, r = 5 meaning every suffix): popc(mh | (b ^ eL))
+// <= r, i.e. lane L's candidates within r of the window when mh = L ^ eH.  mh
+// is the fastest index, so the 32 lanes of a broadcast hit read 32 distinct
+// banks.
 constexpr int kTR = 6;                            // r in [0, 5]
 constexpr int kTWords = kTR * 32 * 32;            // 6144 words (24 KB)
 
 __device__ __forceinline__ void build_suffix_table(uint32_t* T) {
     for (int idx = threadIdx.x; idx < kTWords; idx += blockDim.x) {
-        const uint32_t eL = idx & 31, mh = (idx >> 5) & 31;
+        const uint32_t mh = idx & 31, eL = (idx >> 5) & 31;
         const int r = idx >> 10;
         uint32_t word = 0;
         for (uint32_t b = 0; b < 32; ++b)
@@ -271,12 +273,12 @@ __device__ __forceinline__ void build_suffix_table(uint32_t* T) {
 
 constexpr int kBlockB = 512;  // max threads per CTA of the block kernel
 
-// Hit record made by the lane that found the window: v = r << 10 | eH << 5 |
-// eL with r = min(d - p, 5) the suffix budget and (eH, eL) the window suffix
-// planes.  Lane L's table index is then v ^ (L << 5): row r, mh = eH ^ L, eL.
+// Hit record made by the lane that found the window: v = r << 10 | eL << 5 |
+// eH with r = min(d - p, 5) the suffix budget and (eH, eL) the window suffix
+// planes.  Lane L's table index is then v ^ L: row r, eL, mh = eH ^ L.
 __device__ __forceinline__ uint32_t hit_record(uint32_t w, uint32_t p2, uint32_t d2) {
     const uint32_t r = min((d2 - p2) >> 1, 5u);
-    return (r << 10) | (((w >> 16) & 31u) << 5) | (w & 31u);
+    return (r << 10) | ((w & 31u) << 5) | ((w >> 16) & 31u);
 }
 
 // Process every pending hit of every lane (hm bits index the lane's windows
@@ -284,11 +286,10 @@ __device__ __forceinline__ uint32_t hit_record(uint32_t w, uint32_t p2, uint32_t
 // hit with no suffix budget left (p == d, ~80 % of hits) matches exactly one
 // candidate -- the window's own suffix, lane eH bit eL -- which the finding
 // lane sets in the warp's shared-memory mask with one atomic OR; hits with
-// budget >= 1 are broadcast (one SHFL) and every lane ORs T[v ^ (lane << 5)].
+// budget >= 1 are broadcast (one SHFL) and every lane ORs T[v ^ lane].
 __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uint32_t cb,
                                            uint32_t d2, int lane, const uint32_t* T,
                                            uint32_t* wmask, uint32_t& acc) {
-    const uint32_t lane5 = (uint32_t)lane << 5;
     while (__any_sync(kFull, hm != 0u)) {
         uint32_t mine = kFull;
         if (hm) {
@@ -306,7 +307,7 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uin
         while (who) {
             const int src = __ffs(who) - 1;
             who &= who - 1;
-            acc |= T[__shfl_sync(kFull, mine, src) ^ lane5];
+            acc |= T[__shfl_sync(kFull, mine, src) ^ (uint32_t)lane];
         }
     }
     __syncwarp();
