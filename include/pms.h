@@ -173,6 +173,10 @@ int pms_roofline(int32_t iters, double *compares_per_s,
 /* Static description of a status code. */
 const char *pms_strerror(int status);
 
+/* Where the last PMS_E_CUDA on the calling host thread came from (source
+ * line and CUDA error string); "" if none.  Owned by the library. */
+const char *pms_last_error(void);
+
 /* Number of SMs and the opt-in shared memory per block of the current
  * device (for reporting); PMS_E_CUDA without a device. */
 int pms_device_info(int32_t *sms, int32_t *smem_optin_bytes,

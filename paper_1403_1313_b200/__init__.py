@@ -27,8 +27,9 @@ __all__ = ["find", "find_ex", "Plan", "Launch", "Stats", "roofline", "device_inf
 class PmsError(RuntimeError):
     def __init__(self, status: int, what: str = ""):
         self.status = status
-        super().__init__(f"{what}: {strerror(status)} (status {status})" if what else
-                         f"{strerror(status)} (status {status})")
+        detail = f" [{last_error()}]" if status == E_CUDA else ""
+        super().__init__(f"{what}: {strerror(status)} (status {status}){detail}" if what else
+                         f"{strerror(status)} (status {status}){detail}")
 
 
 class Launch(ctypes.Structure):
@@ -86,6 +87,8 @@ def load() -> ctypes.CDLL:
         lib.pms_roofline.restype = ctypes.c_int
         lib.pms_strerror.argtypes = [ctypes.c_int]
         lib.pms_strerror.restype = ctypes.c_char_p
+        lib.pms_last_error.argtypes = []
+        lib.pms_last_error.restype = ctypes.c_char_p
         lib.pms_device_info.argtypes = [ctypes.POINTER(i32)] * 3
         lib.pms_device_info.restype = ctypes.c_int
         _lib = lib
@@ -94,6 +97,11 @@ def load() -> ctypes.CDLL:
 
 def strerror(status: int) -> str:
     return load().pms_strerror(int(status)).decode()
+
+
+def last_error() -> str:
+    """Source line + CUDA error string of this thread's last PMS_E_CUDA."""
+    return load().pms_last_error().decode()
 
 
 def _rows(seqs) -> np.ndarray:

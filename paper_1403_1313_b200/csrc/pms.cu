@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -37,6 +38,16 @@ namespace {
 constexpr int kSub = 256;          // candidates per aligned sub-block (4 low digits)
 constexpr int kBlock = 256;        // threads per CTA (8 warps)
 constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// Diagnostics for PMS_E_CUDA: the source line and the CUDA error string of the
+// last failure on this host thread (pms_last_error).
+thread_local char g_last_error[256] = "";
+int fail_cuda(int line, cudaError_t e = cudaSuccess) {
+    if (e == cudaSuccess) e = cudaPeekAtLastError();
+    snprintf(g_last_error, sizeof(g_last_error), "pms.cu:%d: %s", line,
+             e == cudaSuccess ? "(no CUDA error pending)" : cudaGetErrorString(e));
+    return PMS_E_CUDA;
+}
 
 // bit-plane word of every 4-digit value i (the low 4 digits of a candidate)
 __constant__ uint32_t c_bp256[kSub];
@@ -321,10 +332,14 @@ __device__ __forceinline__ uint32_t sfx_code(uint32_t h5, uint32_t l5) {
     return (spread_even(h5) << 1) | spread_even(l5);
 }
 
-// NW > 0: lane keeps windows lane + 32j (j < NW) of sequence 0 in registers,
-// pre-masked (suffix bits cleared) and pre-rotated; rows are padded to 32*NW.
+// NW > 0: rows are padded to 32*NW windows and the window loops are fully
+// unrolled; for NW <= kReg0Max the lane also keeps windows lane + 32j of
+// sequence 0 in registers, pre-masked (suffix bits cleared) and pre-rotated
+// (larger NW would cost occupancy: all sequences then stream from smem).
+constexpr int kReg0Max = 24;
 template <bool SMEM, int NW>
-__global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(SearchArgs a) {
+__global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
+    constexpr bool kReg0 = NW > 0 && NW <= kReg0Max;
     extern __shared__ __align__(128) uint32_t stab[];  // [T][table if SMEM]
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t wmasks[kBlockB / 32][32];  // per-warp single-candidate hit masks
@@ -350,9 +365,9 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
     if (SMEM) mbar_wait(&bar, 0);
     const uint32_t* tab = SMEM ? tsm : a.tab;
     const int lane = threadIdx.x & 31;
-    uint32_t wm[NW > 0 ? NW : 1], wmr[NW > 0 ? NW : 1];
+    uint32_t wm[kReg0 ? NW : 1], wmr[kReg0 ? NW : 1];
 #pragma unroll
-    for (int j = 0; j < NW; ++j) {
+    for (int j = 0; j < (kReg0 ? NW : 0); ++j) {
         wm[j] = tab[min(lane + 32 * j, a.W - 1)] & ~kSfxBits;
         wmr[j] = rot16(wm[j]);
     }
@@ -386,9 +401,9 @@ __global__ void __launch_bounds__(kBlockB, (NW > 24 ? 1 : 2)) pms_search_block(S
                 // pass 1: prefix distance of each window; hits recorded per lane
                 if (NW > 0) {
                     uint32_t hm = 0;
-                    if (i == 0) {
+                    if (kReg0 && i == 0) {
 #pragma unroll
-                        for (int j = 0; j < NW; ++j)
+                        for (int j = 0; j < (kReg0 ? NW : 0); ++j)
                             if (__popc((cb ^ wm[j]) | (cr ^ wmr[j])) <= a.d2) hm |= 1u << j;
                     } else {
 #pragma unroll
@@ -520,11 +535,11 @@ bool pick_reg_kernel(int W, int force_g, RegKernel* best) {
 int ensure_constants() {
     static thread_local int dev_done[64] = {0};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return PMS_E_CUDA;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail_cuda(__LINE__);
     if (dev_done[dev]) return PMS_OK;
     uint32_t h[kSub];
     for (int i = 0; i < kSub; ++i) h[i] = code_to_bp((uint32_t)i);
-    if (cudaMemcpyToSymbol(c_bp256, h, sizeof(h)) != cudaSuccess) return PMS_E_CUDA;
+    if (cudaMemcpyToSymbol(c_bp256, h, sizeof(h)) != cudaSuccess) return fail_cuda(__LINE__);
     dev_done[dev] = 1;
     return PMS_OK;
 }
@@ -579,7 +594,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     int st = check_shape(n, t, l, d);
     if (st != PMS_OK) return st;
     pms_plan* p = new (std::nothrow) pms_plan();
-    if (!p) return PMS_E_CUDA;
+    if (!p) return fail_cuda(__LINE__);
     p->n = n; p->t = t; p->l = l; p->d = d;
     p->W = t - l + 1;
     p->Wp = (p->W + 31) / 32 * 32;
@@ -591,7 +606,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
             cudaSuccess ||
         ensure_constants() != PMS_OK) {
         destroy_plan(p);
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     }
     const bool block_algo = (p->launch.algo == PMS_ALGO_BLOCK || p->launch.algo == PMS_ALGO_AUTO) &&
                             !p->launch.no_skip && l >= kBlkS;
@@ -628,10 +643,16 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     p->block = p->launch.warps_per_cta > 0 ? 32 * std::min(p->launch.warps_per_cta, 32)
                                            : (p->algo == PMS_ALGO_BLOCK ? kBlockB : kBlock);
     if (p->block > max_block) p->block = max_block;
-    if (cudaFuncSetAttribute((const void*)p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)p->smem_bytes) != cudaSuccess) {
+    // The attribute is per kernel, shared by every plan (and pooled context)
+    // that launches it: raise it to the device maximum, never to this plan's
+    // size, or a later smaller plan would break an earlier larger one.
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, (const void*)p->fn) != cudaSuccess ||
+        p->smem_bytes + fa.sharedSizeBytes > (size_t)smem_optin ||
+        cudaFuncSetAttribute((const void*)p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem_optin - (int)fa.sharedSizeBytes) != cudaSuccess) {
         destroy_plan(p);
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     }
     int occ = 0;
     if (p->algo == PMS_ALGO_BLOCK && p->launch.warps_per_cta <= 0) {
@@ -650,7 +671,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     }
     if (occ < 1) {
         destroy_plan(p);
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     }
     if (p->launch.ctas_per_sm > 0) occ = std::min(occ, (int)p->launch.ctas_per_sm);
     p->grid = p->sms * occ;
@@ -659,12 +680,12 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         cudaMalloc(&p->d_state, sizeof(DevState)) != cudaSuccess ||
         cudaMallocHost(&p->h_state, sizeof(DevState)) != cudaSuccess) {
         destroy_plan(p);
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     }
     for (cudaEvent_t& e : p->ev)
         if (cudaEventCreate(&e) != cudaSuccess) {
             destroy_plan(p);
-            return PMS_E_CUDA;
+            return fail_cuda(__LINE__);
         }
     *plan = p;
     return PMS_OK;
@@ -703,31 +724,33 @@ extern "C" int pms_plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo,
     a.st = p->d_state; a.nout = reinterpret_cast<unsigned long long*>(d_count);
     a.out = d_out; a.cap = cap;
 
-    if (cudaEventRecord(p->ev[0], s) != cudaSuccess) return PMS_E_CUDA;
+    if (cudaEventRecord(p->ev[0], s) != cudaSuccess) return fail_cuda(__LINE__);
     if (cudaMemsetAsync(p->d_state, 0, sizeof(DevState), s) != cudaSuccess ||
         cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s) != cudaSuccess)
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     const long long cells = (long long)p->n * p->Wp;
     pms_pack_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(d_seqs, p->n, p->t, p->l, p->W,
                                                                      p->Wp, p->d_table, p->d_state);
-    if (cudaGetLastError() != cudaSuccess) return PMS_E_CUDA;
-    if (cudaEventRecord(p->ev[1], s) != cudaSuccess) return PMS_E_CUDA;
+    const cudaError_t e_pack = cudaGetLastError();
+    if (e_pack != cudaSuccess) return fail_cuda(__LINE__, e_pack);
+    if (cudaEventRecord(p->ev[1], s) != cudaSuccess) return fail_cuda(__LINE__);
     if (span > 0) {
         p->fn<<<p->grid, p->block, p->smem_bytes, s>>>(a);
-        if (cudaGetLastError() != cudaSuccess) return PMS_E_CUDA;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail_cuda(__LINE__, e);
     }
-    if (cudaEventRecord(p->ev[2], s) != cudaSuccess) return PMS_E_CUDA;
+    if (cudaEventRecord(p->ev[2], s) != cudaSuccess) return fail_cuda(__LINE__);
     if (cudaMemcpyAsync(p->h_state, p->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s) !=
         cudaSuccess)
-        return PMS_E_CUDA;
-    if (cudaEventRecord(p->ev[3], s) != cudaSuccess) return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
+    if (cudaEventRecord(p->ev[3], s) != cudaSuccess) return fail_cuda(__LINE__);
     p->executed = true;
     return PMS_OK;
 }
 
 extern "C" int pms_plan_wait(pms_plan* p, pms_stats* stats) {
     if (!p || !p->executed) return PMS_E_ARG;
-    if (cudaEventSynchronize(p->ev[3]) != cudaSuccess) return PMS_E_CUDA;
+    if (cudaEventSynchronize(p->ev[3]) != cudaSuccess) return fail_cuda(__LINE__);
     if (stats) {
         float pack = 0.f, search = 0.f, tot = 0.f;
         cudaEventElapsedTime(&pack, p->ev[0], p->ev[1]);
@@ -808,7 +831,7 @@ void ctx_destroy(CallCtx* c) {
 
 int ctx_acquire(int32_t n, int32_t t, int32_t l, int32_t d, const pms_launch& L, CallCtx** out) {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return PMS_E_CUDA;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail_cuda(__LINE__);
     {
         std::lock_guard<std::mutex> lk(g_pool_mu);
         for (size_t i = 0; i < g_pool.size(); ++i)
@@ -819,7 +842,7 @@ int ctx_acquire(int32_t n, int32_t t, int32_t l, int32_t d, const pms_launch& L,
             }
     }
     CallCtx* c = new (std::nothrow) CallCtx();
-    if (!c) return PMS_E_CUDA;
+    if (!c) return fail_cuda(__LINE__);
     c->dev = dev; c->n = n; c->t = t; c->l = l; c->d = d; c->launch = L;
     int st = pms_plan_create(n, t, l, d, &L, &c->plan);
     if (st != PMS_OK) {
@@ -831,7 +854,7 @@ int ctx_acquire(int32_t n, int32_t t, int32_t l, int32_t d, const pms_launch& L,
         cudaMallocHost(&c->h_count, sizeof(uint64_t)) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
         ctx_destroy(c);
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     }
     *out = c;
     return PMS_OK;
@@ -881,14 +904,14 @@ extern "C" int pms_find_ex(const uint8_t* seqs, int32_t n, int32_t t, int32_t l,
         c->out_cap = 0;
         if (cudaMalloc(&c->d_out, cap * sizeof(uint32_t)) != cudaSuccess) {
             healthy = false;
-            return PMS_E_CUDA;
+            return fail_cuda(__LINE__);
         }
         c->out_cap = cap;
     }
     cudaStream_t s = c->stream;
     if (cudaMemcpyAsync(c->d_seqs, seqs, (size_t)n * t, cudaMemcpyHostToDevice, s) != cudaSuccess) {
         healthy = false;
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     }
     st = pms_plan_execute(c->plan, c->d_seqs, lo, hi, c->d_out, cap, c->d_count, s);
     if (st != PMS_OK) {
@@ -898,12 +921,12 @@ extern "C" int pms_find_ex(const uint8_t* seqs, int32_t n, int32_t t, int32_t l,
     if (cudaMemcpyAsync(c->h_count, c->d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
         cudaSuccess) {
         healthy = false;
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     }
     st = pms_plan_wait(c->plan, stats);
     if (cudaStreamSynchronize(s) != cudaSuccess) {
         healthy = false;
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     }
     if (st == PMS_E_CUDA) healthy = false;
     if (st != PMS_OK) return st;
@@ -917,7 +940,7 @@ extern "C" int pms_find_ex(const uint8_t* seqs, int32_t n, int32_t t, int32_t l,
                             s) != cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess) {
             healthy = false;
-            return PMS_E_CUDA;
+            return fail_cuda(__LINE__);
         }
         std::sort(out_codes, out_codes + found);
     }
@@ -939,7 +962,7 @@ extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compa
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev) != cudaSuccess ||
         ensure_constants() != PMS_OK)
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     uint32_t h[G * NW];
     uint32_t x = 0x9E3779B9u;
     for (int i = 0; i < G * NW; ++i) {  // arbitrary 15-mer windows
@@ -951,7 +974,7 @@ extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compa
     if (cudaMalloc(&tab, sizeof(h)) != cudaSuccess ||
         cudaMalloc(&sink, sizeof(unsigned long long)) != cudaSuccess) {
         cudaFree(tab);
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     }
     cudaMemcpy(tab, h, sizeof(h), cudaMemcpyHostToDevice);
     int occ = 0;
@@ -976,7 +999,7 @@ extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compa
     cudaEventDestroy(e1);
     cudaFree(tab);
     cudaFree(sink);
-    if (err != cudaSuccess) return PMS_E_CUDA;
+    if (err != cudaSuccess) return fail_cuda(__LINE__);
     // compares per launch: warps * (iters / CPI) iterations * 32 lanes * NW slots
     const double warps = (double)grid * (kBlock / 32);
     const double cmp = warps * ((double)iters / (32 / G)) * 32.0 * NW;
@@ -985,6 +1008,8 @@ extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compa
     if (ms) *ms = best;
     return PMS_OK;
 }
+
+extern "C" const char* pms_last_error(void) { return g_last_error; }
 
 extern "C" const char* pms_strerror(int status) {
     switch (status) {
@@ -1004,7 +1029,7 @@ extern "C" int pms_device_info(int32_t* sms, int32_t* smem_optin_bytes, int32_t*
         cudaDeviceGetAttribute(&a, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&b, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&c, cudaDevAttrClockRate, dev) != cudaSuccess)
-        return PMS_E_CUDA;
+        return fail_cuda(__LINE__);
     if (sms) *sms = a;
     if (smem_optin_bytes) *smem_optin_bytes = b;
     if (clock_khz) *clock_khz = c;

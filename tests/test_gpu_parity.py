@@ -387,3 +387,19 @@ def test_concurrent_host_calls_and_context_reuse(orc):
     assert gpu(inputs[0], 8, 2).codes.tolist() == want[0]
     assert gpu(inputs[0], 8, 2, lo=5000, hi=9000).codes.tolist() == \
         orc.find(inputs[0], 8, 2, lo=5000, hi=9000).codes.tolist()
+
+
+def test_pooled_plans_sharing_a_kernel(orc):
+    """Regression: two shapes that launch the same kernel instance with
+    different dynamic shared memory; the larger one is reused after the
+    smaller one was created (the per-kernel smem attribute must not shrink)."""
+    big = fmgen.random_sequences(9, 48, 1)    # l=7: W=42 -> same block kernel, 9 rows
+    small = fmgen.random_sequences(2, 48, 2)  # 2 rows
+    for algo in (pms.ALGO_BLOCK, pms.ALGO_CANDIDATE):
+        L = pms.Launch(algo=algo)
+        r1 = gpu(big, 7, 2, launch=L)
+        r2 = gpu(small, 7, 2, launch=L)
+        r3 = gpu(big, 7, 2, launch=L)
+        assert r1.status == r2.status == r3.status == 0, pms.last_error()
+        assert r1.codes.tolist() == r3.codes.tolist() == orc.find(big, 7, 2).codes.tolist()
+        assert r2.codes.tolist() == orc.find(small, 7, 2).codes.tolist()
