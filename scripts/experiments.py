@@ -34,7 +34,12 @@ PAPER_TABLE2 = {  # PAPER.md:130-134 (speedup over 1 thread; other hardware, con
     (14, 4): (23.156, 33.537), (15, 4): (23.608, 38.348)}
 
 
+ALGO = pms.ALGO_AUTO
+
+
 def kernel_ms(seqs, l, d, launch=None, reps=3):
+    if launch is None:
+        launch = pms.Launch(algo=ALGO)
     best, codes = None, None
     for _ in range(reps):
         r = pms.find_ex(seqs, l, d, launch=launch, max_out=1 << 22)
@@ -49,12 +54,17 @@ def kernel_ms(seqs, l, d, launch=None, reps=3):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_experiments"))
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--algo", choices=["auto", "candidate", "block"], default="auto")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
+    global ALGO
+    ALGO = {"auto": pms.ALGO_AUTO, "candidate": pms.ALGO_CANDIDATE, "block": pms.ALGO_BLOCK}[args.algo]
+    if args.out is None:
+        args.out = os.path.join(ROOT, "profiles", f"r01_experiments_{args.algo}")
     pms.build()
-    res = {"device": pms.device_info(), "lsweep": [], "paper_instances": [], "workers": {},
-           "cpu_threads": {}}
+    res = {"device": pms.device_info(), "algo": args.algo, "lsweep": [], "paper_instances": [],
+           "workers": {}, "cpu_threads": {}}
 
     # 1. l-sweep at d = 3 and the paper's instances
     for l in range(9, 17):
@@ -81,10 +91,11 @@ def main():
     for l, d in inst:
         s, codes, full_grid = base[(l, d)]
         workers = [w for w in (1, 2, 4, 8, 16, 32, 64, 148, full_grid)
-                   if not (l == 15 and w < 8)]
+                   if not (l == 15 and w < 8 and ALGO == pms.ALGO_CANDIDATE)]
         rows = []
         for w in sorted(set(workers)):
-            ms, c, st = kernel_ms(s, l, d, launch=pms.Launch(grid_ctas=w), reps=1 if w < 8 else 2)
+            ms, c, st = kernel_ms(s, l, d, launch=pms.Launch(grid_ctas=w, algo=ALGO),
+                                  reps=1 if w < 8 else 2)
             assert c == codes, "motif set depends on the number of workers"
             rows.append({"ctas": st.grid, "search_ms": ms})
         t1 = rows[0]["search_ms"] * rows[0]["ctas"]  # normalise to 1 CTA if 1 was skipped
@@ -114,7 +125,7 @@ def main():
 
     json.dump(res, open(args.out + ".json", "w"), indent=1)
     # Table II layout
-    lines = ["# Paper-experiment analogues on B200 (scripts/experiments.py)", "",
+    lines = [f"# Paper-experiment analogues on B200 (scripts/experiments.py --algo {args.algo})", "",
              "## Fig. 2 analogue: search-kernel time vs l (d = 3, n=20, t=600, seed 1)", "",
              "| l | kernel ms | ratio to l-1 | candidates/s | motifs |", "|---|---|---|---|---|"]
     for r in res["lsweep"]:
