@@ -66,16 +66,19 @@ typedef struct pms_launch {
                                 "enhanced version"): every candidate scans all
                                 n sequences; same result, n*W compares each  */
     int32_t algo;            /* PMS_ALGO_*: which kernel family (0 = auto)   */
+    int32_t block_digits;    /* PMS_ALGO_BLOCK suffix digits S (5: 1024-, 6:
+                                4096-candidate blocks); 0 = auto (6 if l >= 13)*/
+    int32_t reserved[3];
 } pms_launch;
 
 /* Kernel families (pms_launch.algo).  Every family returns the same set.
  *   PMS_ALGO_CANDIDATE: one candidate per 16/32 lanes; each candidate-window
  *     Hamming test is XOR, XOR-OR fold, POPC.
- *   PMS_ALGO_BLOCK: the 1024 candidates sharing their first l-5 digits are
- *     tested together (bit-parallel over candidates): one XOR/fold/POPC of the
- *     shared prefix against a window gives the prefix distance p, and the
- *     candidates whose last 5 digits lie within d-p of the window's last 5
- *     digits match that window (a Hamming-ball bitmask).  Each candidate keeps
+ *   PMS_ALGO_BLOCK: the 4^S candidates sharing their first l-S digits (S = 5
+ *     or 6) are tested together (bit-parallel over candidates): one
+ *     XOR/fold/POPC of the shared prefix against a window gives the prefix
+ *     distance p, and the candidates whose last S digits lie within d-p of the
+ *     window's last S digits match that window (a Hamming-ball bitmask).  Each candidate keeps
  *     PAPER.md:63's semantics: it is compared with the windows of sequence
  *     0, 1, ... and dropped at the first sequence with no window within d; the
  *     block is abandoned when no candidate is left (the skip rule on 1024
@@ -97,8 +100,10 @@ typedef struct pms_stats {
     uint32_t smem_bytes;
     int32_t algo;              /* PMS_ALGO_* actually run                    */
     uint64_t block_scans;      /* PMS_ALGO_BLOCK: (block, sequence) scans;
-                                  each is W prefix compares serving 256
+                                  each is W prefix compares serving 4^S
                                   candidates                                 */
+    int32_t block_digits;      /* PMS_ALGO_BLOCK suffix digits S (0 if none) */
+    int32_t reserved;
 } pms_stats;
 
 /* ---------------------------------------------------------------------

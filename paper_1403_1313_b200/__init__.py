@@ -36,7 +36,8 @@ class Launch(ctypes.Structure):
     _fields_ = [("ctas_per_sm", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32),
                 ("batch", ctypes.c_int32), ("lanes_per_cand", ctypes.c_int32),
                 ("force_generic", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
-                ("no_skip", ctypes.c_int32), ("algo", ctypes.c_int32)]
+                ("no_skip", ctypes.c_int32), ("algo", ctypes.c_int32),
+                ("block_digits", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class Stats(ctypes.Structure):
@@ -47,7 +48,8 @@ class Stats(ctypes.Structure):
                 ("lanes_per_cand", ctypes.c_int32), ("windows_per_lane", ctypes.c_int32),
                 ("generic", ctypes.c_int32), ("table_in_smem", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_uint32), ("algo", ctypes.c_int32),
-                ("block_scans", ctypes.c_uint64)]
+                ("block_scans", ctypes.c_uint64), ("block_digits", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -243,93 +243,112 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
 }
 
 // ------------------------------------------------- PMS_ALGO_BLOCK search
-// The 1024 candidates of a 1024-aligned code block share their first l-5
-// digits (the prefix P) and differ in the last 5 (the suffix x).  For a
-// window w, Hamming(P x, w) = Hamming(P, w[0..l-5)) + Hamming(x, w[l-5..l)),
-// so one XOR / XOR-OR fold / POPC of the prefix against w gives p, and the
-// block candidates that match w (distance <= d) are exactly the
-// suffixes within Hamming distance d - p of w's suffix.  Lane L of the warp
-// owns the 32 candidates x = 32L + b: a window with p <= d (a "hit", ~2 % of
-// windows at (15,4)) is broadcast to all lanes (one SHFL), and every lane ORs
-// the matching bits of its own word, read from a 2 KB table.  After a
-// sequence, alive &= acc; the block is abandoned at the first sequence that
-// leaves no candidate alive -- the skip rule on 1024 candidates at once -- and
-// a lone survivor is finished by the whole warp (check_sequences).
-constexpr int kBlkS = 5;                    // suffix digits per block
-constexpr int kBlkC = 1 << (2 * kBlkS);     // 1024 candidates per block
-constexpr uint32_t kSfxBits = 0x001F001Fu;  // suffix positions in both planes
-constexpr int kUnit = kBlkC;                // batch / lo alignment (multiple of kSub)
+// The 4^S candidates of a 4^S-aligned code block (S = 5 or 6) share their
+// first l-S digits (the prefix P) and differ in the last S (the suffix x).
+// For a window w, Hamming(P x, w) = Hamming(P, w[0..l-S)) + Hamming(x,
+// w[l-S..l)), so one XOR / XOR-OR fold / POPC of the prefix against w gives p,
+// and the block candidates that match w (distance <= d) are
+// exactly the suffixes within Hamming distance d - p of w's suffix.  After a
+// sequence, alive &= acc (the candidates with a window within d in it); the
+// block is abandoned at the first sequence that leaves no candidate alive --
+// the skip rule on 4^S candidates at once -- and a lone survivor is finished
+// by the whole warp (check_sequences).
+//
+// Candidates are indexed in BIT-PLANE order.  A suffix has planes (H, L) of S
+// bits (H = high bits, L = low bits of its base codes, position l-S in bit
+// S-1); its distance to a window suffix (eH, eL) is popc((H ^ eH) | (L ^ eL)).
+// With X = S - 5: lane = H >> X, mask word k = (H & (2^X-1)) << X | (L >> 5)
+// (4^X words per lane), bit = L & 31.
+//   * a hit with no budget left (p == d, ~80 % of hits) matches only the
+//     window's own suffix: the finding lane sets bit eL & 31 of word
+//     (eH << X) | (eL >> 5) of the warp's shared-memory mask (one atomic OR);
+//   * other hits are broadcast (one SHFL) and every lane ORs, per word, the
+//     table entry T[r-1][eL & 31][mm] with mm = (H ^ eH) | ((L >> 5 ^ eL >> 5) << 5):
+//     bit b set iff popc(mm | (b ^ (eL & 31))) <= r.  mm is the fastest index,
+//     so a broadcast reads (nearly) distinct banks.
+constexpr int kUnit = 4096;                 // batch / lo alignment (largest block)
 static_assert(kUnit % kSub == 0, "batches hold whole 256-candidate sub-blocks");
-// Candidates of a block are indexed in BIT-PLANE order: the block candidate
-// with suffix planes (H5, L5) -- H5 = high bits, L5 = low bits of its last 5
-// base codes, position l-5 in bit 4 -- is owned by lane H5, bit L5.  Its
-// distance to a window suffix (eH, eL) is popc((H5 ^ eH) | (L5 ^ eL)).
-// T[r][eL][mh] bit b (r in 0..5, r = 5 meaning every suffix): popc(mh | (b ^ eL))
-// <= r, i.e. lane L's candidates within r of the window when mh = L ^ eH.  mh
-// is the fastest index, so the 32 lanes of a broadcast hit read 32 distinct
-// banks.
-constexpr int kTR = 6;                            // r in [0, 5]
-constexpr int kTWords = kTR * 32 * 32;            // 6144 words (24 KB)
+constexpr int kBlockB = 512;                // max threads per CTA of the block kernel
+constexpr int kBlkMinL = 5;                 // the block family needs l >= 5
 
+template <int S>
+struct BlkTraits {
+    static constexpr int X = S - 5;
+    static constexpr int C = 1 << (2 * S);               // candidates per block
+    static constexpr int KW = 1 << (2 * X);              // mask words per lane
+    static constexpr uint32_t M = (1u << S) - 1u;        // suffix plane mask
+    static constexpr uint32_t SFX = M | (M << 16);       // suffix bits of a word
+    static constexpr int TROW = 32 << S;                 // words per budget row
+    static constexpr int TWORDS = S * TROW;              // rows r = 1..S (r = S: all)
+};
+
+template <int S>
 __device__ __forceinline__ void build_suffix_table(uint32_t* T) {
-    for (int idx = threadIdx.x; idx < kTWords; idx += blockDim.x) {
-        const uint32_t mh = idx & 31, eL = (idx >> 5) & 31;
-        const int r = idx >> 10;
+    using B = BlkTraits<S>;
+    for (int idx = threadIdx.x; idx < B::TWORDS; idx += blockDim.x) {
+        const uint32_t mm = idx & B::M, eL = (idx >> S) & 31;
+        const int r = idx / B::TROW + 1;
         uint32_t word = 0;
         for (uint32_t b = 0; b < 32; ++b)
-            if ((int)__popc(mh | (b ^ eL)) <= r) word |= 1u << b;
+            if ((int)__popc(mm | (b ^ eL)) <= r) word |= 1u << b;
         T[idx] = word;
     }
 }
 
-constexpr int kBlockB = 512;  // max threads per CTA of the block kernel
-
-// Hit record made by the lane that found the window: v = r << 10 | eL << 5 |
-// eH with r = min(d - p, 5) the suffix budget and (eH, eL) the window suffix
-// planes.  Lane L's table index is then v ^ L: row r, eL, mh = eH ^ L.
-__device__ __forceinline__ uint32_t hit_record(uint32_t w, uint32_t p2, uint32_t d2) {
-    const uint32_t r = min((d2 - p2) >> 1, 5u);
-    return (r << 10) | ((w & 31u) << 5) | ((w >> 16) & 31u);
+// Suffix code (S digits, big-endian base 4) of the suffix with planes (H, L).
+__device__ __forceinline__ uint32_t sfx_code(uint32_t h, uint32_t l) {
+    return (spread_even(h) << 1) | spread_even(l);
 }
 
 // Process every pending hit of every lane (hm bits index the lane's windows
-// row[lane + 32*j]) and OR the matching candidates into each lane's acc.  A
-// hit with no suffix budget left (p == d, ~80 % of hits) matches exactly one
-// candidate -- the window's own suffix, lane eH bit eL -- which the finding
-// lane sets in the warp's shared-memory mask with one atomic OR; hits with
-// budget >= 1 are broadcast (one SHFL) and every lane ORs T[v ^ lane].
+// row[lane + 32*j]) and OR the matching candidates into the lane's acc words.
+template <int S>
 __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uint32_t cb,
                                            uint32_t d2, int lane, const uint32_t* T,
-                                           uint32_t* wmask, uint32_t& acc) {
+                                           uint32_t* wmask,
+                                           uint32_t (&acc)[BlkTraits<S>::KW]) {
+    using B = BlkTraits<S>;
     while (__any_sync(kFull, hm != 0u)) {
         uint32_t mine = kFull;
         if (hm) {
             const int j = __ffs(hm) - 1;
             hm &= hm - 1;
             const uint32_t w = row[lane + 32 * j];
-            const uint32_t x = (cb ^ w) & ~kSfxBits;
+            const uint32_t x = (cb ^ w) & ~B::SFX;
             const uint32_t p2 = __popc(x | rot16(x));
-            if (p2 == d2)
-                atomicOr(&wmask[(w >> 16) & 31u], 1u << (w & 31u));
-            else
-                mine = hit_record(w, p2, d2);
+            const uint32_t eH = (w >> 16) & B::M, eL = w & B::M;
+            if (p2 == d2) {
+                atomicOr(&wmask[(eH << B::X) | (eL >> 5)], 1u << (eL & 31u));
+            } else {  // record: (r-1) row, eL & 31, eH in the low S bits, eL >> 5 on top
+                const uint32_t r = min((d2 - p2) >> 1, (uint32_t)S);
+                mine = ((((r - 1) << 5) | (eL & 31u)) << S) | eH | ((eL >> 5) << 24);
+            }
         }
         uint32_t who = __ballot_sync(kFull, mine != kFull);
         while (who) {
             const int src = __ffs(who) - 1;
             who &= who - 1;
-            acc |= T[__shfl_sync(kFull, mine, src) ^ (uint32_t)lane];
+            const uint32_t v = __shfl_sync(kFull, mine, src);
+            if (B::X == 0) {
+                acc[0] |= T[v ^ (uint32_t)lane];
+            } else {
+                const uint32_t vx = v & 0x00FFFFFFu, eLt = v >> 24;
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) {
+                    const uint32_t hk = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
+                    const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
+                    acc[k] |= T[(vx ^ hk) | ((lt ^ eLt) << 5)];
+                }
+            }
         }
     }
     __syncwarp();
-    acc |= wmask[lane];
-    wmask[lane] = 0u;
+#pragma unroll
+    for (int k = 0; k < B::KW; ++k) {
+        acc[k] |= wmask[lane * B::KW + k];
+        wmask[lane * B::KW + k] = 0u;
+    }
     __syncwarp();
-}
-
-// Suffix code (5 digits, big-endian base 4) of block candidate (H5 = lane, L5 = bit).
-__device__ __forceinline__ uint32_t sfx_code(uint32_t h5, uint32_t l5) {
-    return (spread_even(h5) << 1) | spread_even(l5);
 }
 
 // NW > 0: rows are padded to 32*NW windows and the window loops are fully
@@ -337,17 +356,19 @@ __device__ __forceinline__ uint32_t sfx_code(uint32_t h5, uint32_t l5) {
 // sequence 0 in registers, pre-masked (suffix bits cleared) and pre-rotated
 // (larger NW would cost occupancy: all sequences then stream from smem).
 constexpr int kReg0Max = 24;
-template <bool SMEM, int NW>
+template <int S, bool SMEM, int NW>
 __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
+    using B = BlkTraits<S>;
     constexpr bool kReg0 = NW > 0 && NW <= kReg0Max;
     extern __shared__ __align__(128) uint32_t stab[];  // [T][table if SMEM]
     __shared__ __align__(8) uint64_t bar;
-    __shared__ uint32_t wmasks[kBlockB / 32][32];  // per-warp single-candidate hit masks
+    __shared__ uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp single-candidate hits
     if (*(volatile unsigned int*)&a.st->bad) return;
     uint32_t* T = stab;
     uint32_t* wmask = wmasks[threadIdx.x >> 5];
-    wmask[threadIdx.x & 31] = 0u;
-    uint32_t* tsm = stab + kTWords;  // 5 KB: keeps the table 128-B aligned for the bulk copy
+#pragma unroll
+    for (int k = 0; k < B::KW; ++k) wmask[(threadIdx.x & 31) * B::KW + k] = 0u;
+    uint32_t* tsm = stab + B::TWORDS;  // 128-B aligned for the bulk copy
     if (SMEM) {  // start the table's TMA bulk copy, build the suffix table meanwhile
         if (threadIdx.x == 0) mbar_init(&bar, 1);
         __syncthreads();
@@ -360,7 +381,7 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
                              min(kChunk, a.tab_bytes - off), &bar);
         }
     }
-    build_suffix_table(T);
+    build_suffix_table<S>(T);
     __syncthreads();
     if (SMEM) mbar_wait(&bar, 0);
     const uint32_t* tab = SMEM ? tsm : a.tab;
@@ -368,7 +389,7 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
     uint32_t wm[kReg0 ? NW : 1], wmr[kReg0 ? NW : 1];
 #pragma unroll
     for (int j = 0; j < (kReg0 ? NW : 0); ++j) {
-        wm[j] = tab[min(lane + 32 * j, a.W - 1)] & ~kSfxBits;
+        wm[j] = tab[min(lane + 32 * j, a.W - 1)] & ~B::SFX;
         wmr[j] = rot16(wm[j]);
     }
     unsigned long long scanned = 0, bscans = 0;
@@ -378,26 +399,41 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
         if (lane == 0) b = atomicAdd(&a.st->next, (unsigned long long)a.batch);
         b = __shfl_sync(kFull, b, 0);
         if (b >= a.span) break;
-        for (int sb = 0; sb < a.batch; sb += kBlkC) {
+        for (int sb = 0; sb < a.batch; sb += B::C) {
             const unsigned long long cbase = a.lo_al + b + sb;
             if (cbase >= a.hi) break;
             const uint32_t cb = code_to_bp((uint32_t)cbase);  // suffix bits are zero
             const uint32_t cr = rot16(cb);
-            // this lane's 32 candidates (H5 = lane, L5 = bit) inside [lo, hi)
-            uint32_t alive = kFull;
-            if (cbase < a.lo || cbase + kBlkC > a.hi) {  // edge block of [lo, hi)
-                alive = 0u;
-                for (uint32_t bb = 0; bb < 32; ++bb) {
-                    const unsigned long long c = cbase + sfx_code((uint32_t)lane, bb);
-                    if (c >= a.lo && c < a.hi) alive |= 1u << bb;
+            // this lane's candidates inside [lo, hi)
+            uint32_t alive[B::KW];
+#pragma unroll
+            for (int k = 0; k < B::KW; ++k) alive[k] = kFull;
+            if (cbase < a.lo || cbase + B::C > a.hi) {  // edge block of [lo, hi)
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) {
+                    const uint32_t h = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
+                    const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
+                    uint32_t m = 0u;
+                    for (uint32_t bb = 0; bb < 32; ++bb) {
+                        const unsigned long long c = cbase + sfx_code(h, (lt << 5) | bb);
+                        if (c >= a.lo && c < a.hi) m |= 1u << bb;
+                    }
+                    alive[k] = m;
                 }
             }
             int i = 0;
             bool dead = false;
             for (; i < a.n; ++i) {
-                if (i > 0 && __reduce_add_sync(kFull, __popc(alive)) <= 1) break;
+                if (i > 0) {
+                    int na = 0;
+#pragma unroll
+                    for (int k = 0; k < B::KW; ++k) na += __popc(alive[k]);
+                    if (__reduce_add_sync(kFull, na) <= 1) break;
+                }
                 const uint32_t* row = tab + (size_t)i * a.Wp;
-                uint32_t acc = 0;
+                uint32_t acc[B::KW];
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) acc[k] = 0u;
                 // pass 1: prefix distance of each window; hits recorded per lane
                 if (NW > 0) {
                     uint32_t hm = 0;
@@ -408,48 +444,61 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
                     } else {
 #pragma unroll
                         for (int j = 0; j < NW; ++j) {
-                            const uint32_t x = (cb ^ row[lane + 32 * j]) & ~kSfxBits;
+                            const uint32_t x = (cb ^ row[lane + 32 * j]) & ~B::SFX;
                             if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
                         }
                     }
-                    // pass 2: broadcast the hits; each lane ORs its own candidates
-                    drain_hits(hm, row, cb, a.d2, lane, T, wmask, acc);
+                    // pass 2: resolve the hits into each lane's candidate words
+                    drain_hits<S>(hm, row, cb, a.d2, lane, T, wmask, acc);
                 } else {
                     for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
                         uint32_t hm = 0;
                         const int nj = min(a.Wp - k0, 32 * 32) / 32;
                         for (int j = 0; j < nj; ++j) {
-                            const uint32_t x = (cb ^ row[k0 + lane + 32 * j]) & ~kSfxBits;
+                            const uint32_t x = (cb ^ row[k0 + lane + 32 * j]) & ~B::SFX;
                             if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
                         }
-                        drain_hits(hm, row + k0, cb, a.d2, lane, T, wmask, acc);
+                        drain_hits<S>(hm, row + k0, cb, a.d2, lane, T, wmask, acc);
                     }
                 }
-                alive &= acc;
+                uint32_t any = 0;
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) {
+                    alive[k] &= acc[k];
+                    any |= alive[k];
+                }
                 ++bscans;
-                if (!__any_sync(kFull, alive != 0u)) {  // skip rule for the whole block
+                if (!__any_sync(kFull, any != 0u)) {  // skip rule for the whole block
                     dead = true;
                     break;
                 }
             }
             if (dead) continue;
             if (i == a.n) {  // every alive candidate matched all n sequences
-                if (alive) {
-                    const unsigned long long slot0 = atomicAdd(a.nout, (unsigned long long)__popc(alive));
-                    uint32_t m = alive;
-                    for (unsigned long long slot = slot0; m; ++slot) {
-                        const int bit = __ffs(m) - 1;
-                        m &= m - 1;
-                        if (slot < a.cap) a.out[slot] = (uint32_t)(cbase + sfx_code(lane, bit));
-                    }
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) {
+                    if (!alive[k]) continue;
+                    const uint32_t h = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
+                    const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
+                    unsigned long long slot = atomicAdd(a.nout, (unsigned long long)__popc(alive[k]));
+                    for (uint32_t m = alive[k]; m; m &= m - 1, ++slot)
+                        if (slot < a.cap)
+                            a.out[slot] = (uint32_t)(cbase + sfx_code(h, (lt << 5) | (__ffs(m) - 1)));
                 }
                 continue;
             }
             // one survivor left: the whole warp finishes it from sequence i on
-            const uint32_t holder = __ballot_sync(kFull, alive != 0u);
+            uint32_t pick = kFull;  // (k << 5) | bit of this lane's first alive candidate
+#pragma unroll
+            for (int k = B::KW - 1; k >= 0; --k)
+                if (alive[k]) pick = ((uint32_t)k << 5) | (__ffs(alive[k]) - 1);
+            const uint32_t holder = __ballot_sync(kFull, pick != kFull);
             const int src = __ffs(holder) - 1;
-            const uint32_t word = __shfl_sync(kFull, alive, src);
-            const uint32_t code = (uint32_t)(cbase + sfx_code(src, __ffs(word) - 1));
+            const uint32_t pk = __shfl_sync(kFull, pick, src);
+            const uint32_t k = pk >> 5;
+            const uint32_t h = ((uint32_t)src << B::X) | (k >> B::X);
+            const uint32_t l5 = ((k & ((1u << B::X) - 1u)) << 5) | (pk & 31u);
+            const uint32_t code = (uint32_t)(cbase + sfx_code(h, l5));
             if (check_sequences(tab, i, a.n, a.Wp, code_to_bp(code), a.d2, lane, scanned) &&
                 lane == 0)
                 append(a, code);
@@ -463,12 +512,15 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
 
 using BlockFn = void (*)(SearchArgs);
 struct BlockKernel {
-    int NW;
+    int S, NW;
     BlockFn fn_smem, fn_global;
 };
-#define PMS_BLK(nw) {nw, pms_search_block<true, nw>, pms_search_block<false, nw>},
-const BlockKernel kBlockKernels[] = {{0, pms_search_block<true, 0>, pms_search_block<false, 0>},
-                                     PMS_NW_LIST(PMS_BLK)};
+#define PMS_BLK5(nw) {5, nw, pms_search_block<5, true, nw>, pms_search_block<5, false, nw>},
+#define PMS_BLK6(nw) {6, nw, pms_search_block<6, true, nw>, pms_search_block<6, false, nw>},
+const BlockKernel kBlockKernels[] = {
+    {5, 0, pms_search_block<5, true, 0>, pms_search_block<5, false, 0>},
+    {6, 0, pms_search_block<6, true, 0>, pms_search_block<6, false, 0>},
+    PMS_NW_LIST(PMS_BLK5) PMS_NW_LIST(PMS_BLK6)};
 
 // ---------------------------------------------------- roofline microbenchmark
 // The exact per-compare sequence of pms_search_reg<G,NW> (same register-
@@ -558,7 +610,7 @@ struct pms_plan {
     DevState* h_state = nullptr;  // pinned mirror, filled after each execution
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, packed, searched, state copied
     SearchFn fn = nullptr;
-    int G = 32, NW = 0, generic = 0, in_smem = 0, algo = PMS_ALGO_CANDIDATE;
+    int G = 32, NW = 0, generic = 0, in_smem = 0, algo = PMS_ALGO_CANDIDATE, S = 0;
     uint32_t tab_bytes = 0, smem_bytes = 0;
     int grid = 0, block = kBlock, batch = kSub;
     unsigned long long last_lo = 0, last_hi = 0;
@@ -609,18 +661,29 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         return fail_cuda(__LINE__);
     }
     const bool block_algo = (p->launch.algo == PMS_ALGO_BLOCK || p->launch.algo == PMS_ALGO_AUTO) &&
-                            !p->launch.no_skip && l >= kBlkS;
-    const BlockKernel* bk = &kBlockKernels[0];
-    if (block_algo && !p->launch.force_generic)
-        for (const BlockKernel& k : kBlockKernels)  // sequence 0 register-resident
-            if (k.NW > 0 && 32 * k.NW >= p->W) {
-                bk = &k;
-                p->Wp = 32 * k.NW;  // rows padded to the register tile (re-read on hits)
-                break;
-            }
+                            !p->launch.no_skip && l >= kBlkMinL;
+    // block digits S: 6 (4096-candidate blocks) when there are enough blocks to
+    // keep every warp busy (l >= 13: >= 16k blocks), else 5
+    int S = p->launch.block_digits == 5 || p->launch.block_digits == 6 ? p->launch.block_digits
+                                                                        : (l >= 13 ? 6 : 5);
+    if (S > l) S = 5;
+    const BlockKernel* bk = nullptr;
+    if (block_algo) {
+        for (const BlockKernel& k : kBlockKernels)  // generic (NW = 0) of this S first
+            if (k.S == S && k.NW == 0) { bk = &k; break; }
+        if (!p->launch.force_generic)
+            for (const BlockKernel& k : kBlockKernels)  // smallest register tile covering W
+                if (k.S == S && k.NW > 0 && 32 * k.NW >= p->W) {
+                    bk = &k;
+                    p->Wp = 32 * k.NW;  // rows padded to the tile (re-read on hits)
+                    break;
+                }
+        p->S = S;
+    }
     p->tab_bytes = (uint32_t)((size_t)n * p->Wp * 4);
-    const uint32_t static_smem = 4096;  // mbarrier, per-warp hit masks, slack
-    const uint32_t ball_bytes = block_algo ? (uint32_t)kTWords * 4u : 0u;  // suffix table
+    const uint32_t static_smem = 12288;  // mbarrier, per-warp hit masks, slack
+    const uint32_t ball_bytes =
+        block_algo ? (uint32_t)(S == 6 ? BlkTraits<6>::TWORDS : BlkTraits<5>::TWORDS) * 4u : 0u;
     p->in_smem = p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
     p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0);
 
@@ -772,6 +835,7 @@ extern "C" int pms_plan_wait(pms_plan* p, pms_stats* stats) {
                                   (p->h_state->extra + p->h_state->block_scans) * W;
         stats->algo = p->algo;
         stats->block_scans = p->h_state->block_scans;
+        stats->block_digits = p->S;
         stats->motifs = 0;
         stats->grid = p->grid;
         stats->block = p->block;

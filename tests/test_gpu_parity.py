@@ -276,18 +276,24 @@ def test_grid_size_override():
 # ------------------------------------------------ PMS_ALGO_BLOCK family
 
 BLOCK = pms.Launch(algo=pms.ALGO_BLOCK)
+BLOCKS = [pms.Launch(algo=pms.ALGO_BLOCK, block_digits=5),
+          pms.Launch(algo=pms.ALGO_BLOCK, block_digits=6)]
 
 
-def test_block_algo_tiny_random(orc):
-    rng = random.Random(4242)
+@pytest.mark.parametrize("S", [5, 6])
+def test_block_algo_tiny_random(orc, S):
+    rng = random.Random(4242 + S)
+    L = pms.Launch(algo=pms.ALGO_BLOCK, block_digits=S)
     for trial in range(80):
         l = rng.randint(1, 9)
         n = rng.randint(1, 5)
         t = rng.randint(l, 90)
-        d = rng.randint(0, min(4, l))
+        d = rng.randint(0, min(5, l))
         s = fmgen.random_sequences(n, t, 7000 + trial)
-        got, _ = assert_same(s, l, d, orc, launch=BLOCK)
+        got, _ = assert_same(s, l, d, orc, launch=L)
         assert got.stats.algo == (pms.ALGO_BLOCK if l >= 5 else pms.ALGO_CANDIDATE)
+        if l >= 5:
+            assert got.stats.block_digits == (S if l >= S else 5)
     # 1024-candidate blocks: l = 5 is a single block with an empty prefix
     for seed in range(5):
         s = fmgen.random_sequences(3, 30, 60 + seed)
@@ -309,16 +315,19 @@ def test_block_algo_planted_and_edges(orc):
     assert_same(s, 7, 2, orc, launch=BLOCK)
 
 
-def test_block_algo_ranges(orc):
+@pytest.mark.parametrize("S", [5, 6])
+def test_block_algo_ranges(orc, S):
+    L = pms.Launch(algo=pms.ALGO_BLOCK, block_digits=S)
     s, _ = fmgen.generate_fm(5, 60, 7, 1, 4)
-    full = gpu(s, 7, 1, launch=BLOCK).codes.tolist()
+    full = gpu(s, 7, 1, launch=L).codes.tolist()
     assert full == orc.find(s, 7, 1).codes.tolist()
     for lo, hi in [(0, 1), (1, 255), (3, 9), (255, 257), (300, 5000), (4095, 4 ** 7),
-                   (16383, 16384), (100, 100), (1023, 1025), (1000, 3100), (31, 33)]:
-        assert_same(s, 7, 1, orc, lo=lo, hi=hi, launch=BLOCK)
+                   (16383, 16384), (100, 100), (1023, 1025), (1000, 3100), (31, 33),
+                   (4095, 4097), (4000, 12300)]:
+        assert_same(s, 7, 1, orc, lo=lo, hi=hi, launch=L)
     for cut in (1, 777, 8192):
-        a = gpu(s, 7, 1, lo=0, hi=cut, launch=BLOCK).codes.tolist()
-        b = gpu(s, 7, 1, lo=cut, hi=4 ** 7, launch=BLOCK).codes.tolist()
+        a = gpu(s, 7, 1, lo=0, hi=cut, launch=L).codes.tolist()
+        b = gpu(s, 7, 1, lo=cut, hi=4 ** 7, launch=L).codes.tolist()
         assert a + b == full
 
 
@@ -326,7 +335,8 @@ def test_block_algo_window_counts(orc):
     for W in (1, 31, 33, 586, 985, 2100):
         l, d = 8, 2
         s, _ = fmgen.generate_fm(3, W + l - 1, l, d, W)
-        assert_same(s, l, d, orc, launch=BLOCK)
+        for L in BLOCKS:
+            assert_same(s, l, d, orc, launch=L)
 
 
 def test_block_algo_global_table_and_l16(orc):
@@ -337,7 +347,8 @@ def test_block_algo_global_table_and_l16(orc):
     cons = int("".join(str("ACGT".index(c)) for c in rec.consensus), 4)
     for lo, hi in [(0, 1 << 20), (cons - (1 << 19), cons + (1 << 19)),
                    ((1 << 32) - (1 << 20), 1 << 32)]:
-        assert_same(s, 16, 5, orc, lo=max(lo, 0), hi=min(hi, 1 << 32), launch=BLOCK)
+        for L in BLOCKS:
+            assert_same(s, 16, 5, orc, lo=max(lo, 0), hi=min(hi, 1 << 32), launch=L)
     a = gpu(s, 16, 5, max_out=1 << 26, launch=BLOCK)
     b = gpu(s, 16, 5, max_out=1 << 26)
     assert a.status == b.status == 0 and a.codes.tolist() == b.codes.tolist()
@@ -345,18 +356,19 @@ def test_block_algo_global_table_and_l16(orc):
 
 def test_block_algo_launch_invariance():
     s, _ = fmgen.generate_fm(20, 600, 11, 3, 1)
-    base = gpu(s, 11, 3).codes.tolist()
-    for kw in [dict(), dict(grid_ctas=1), dict(grid_ctas=7), dict(warps_per_cta=3),
-               dict(batch=4096), dict(batch=256)]:
-        L = pms.Launch(algo=pms.ALGO_BLOCK, **kw)
-        assert gpu(s, 11, 3, launch=L).codes.tolist() == base, kw
+    base = gpu(s, 11, 3, launch=CAND).codes.tolist()
+    for S in (5, 6):
+        for kw in [dict(), dict(grid_ctas=1), dict(grid_ctas=7), dict(warps_per_cta=3),
+                   dict(batch=4096), dict(batch=256), dict(batch=12288), dict(force_generic=1)]:
+            L = pms.Launch(algo=pms.ALGO_BLOCK, block_digits=S, **kw)
+            assert gpu(s, 11, 3, launch=L).codes.tolist() == base, (S, kw)
 
 
 @pytest.mark.parametrize("path", GOLDEN_FILES, ids=[os.path.basename(p) for p in GOLDEN_FILES])
 def test_block_algo_baseline_configs(orc, path):
     g = json.load(open(path))
     s, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
-    for launch in (BLOCK, None):  # explicit and the default (AUTO) family
+    for launch in BLOCKS + [None]:  # both block sizes and the default (AUTO) family
         r = gpu(s, g["l"], g["d"], launch=launch)
         assert r.status == 0 and r.stats.algo == pms.ALGO_BLOCK
         assert r.count == g["count"] and r.codes.tolist() == g["codes"]
