@@ -57,7 +57,7 @@ struct SearchArgs {
     int n, W, Wp;
     uint32_t d2;                    // 2*min(d, l): popc(x|rot16(x)) = 2*Hamming
     unsigned long long lo, hi;      // candidate code range [lo, hi)
-    unsigned long long lo_al;       // lo rounded down to kUnit (1024)
+    unsigned long long lo_al;       // lo rounded down to the plan unit (256 or 4^S)
     unsigned long long span;        // hi - lo_al
     int batch;                      // candidates per atomic grab (multiple of kSub)
     int in_smem;                    // stage the table into shared memory (TMA bulk)
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
 //     table entry T[r-1][eL & 31][mm] with mm = (H ^ eH) | ((L >> 5 ^ eL >> 5) << 5):
 //     bit b set iff popc(mm | (b ^ (eL & 31))) <= r.  mm is the fastest index,
 //     so a broadcast reads (nearly) distinct banks.
-constexpr int kUnit = 4096;                 // batch / lo alignment (largest block)
-static_assert(kUnit % kSub == 0, "batches hold whole 256-candidate sub-blocks");
+constexpr int kUnitMax = 4096;              // largest block (S = 6)
+static_assert(kUnitMax % kSub == 0, "batches hold whole 256-candidate sub-blocks");
 constexpr int kBlockB = 512;                // max threads per CTA of the block kernel
 constexpr int kBlkMinL = 5;                 // the block family needs l >= 5
 
@@ -763,16 +763,21 @@ extern "C" int pms_plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo,
     if (hi > total) hi = total;
     if (lo > hi) return PMS_E_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // batches and lo are aligned to the plan's unit: one block (4^S candidates)
+    // for the block family, a 256-candidate sub-block for the candidate family
+    const unsigned long long kUnit =
+        p->algo == PMS_ALGO_BLOCK ? (1ull << (2 * p->S)) : (unsigned long long)kSub;
     const unsigned long long lo_al = lo / kUnit * kUnit;
     const unsigned long long span = hi - lo_al;
 
     // batch: aim for >= 8 grabs per warp, multiple of kSub, at most 16 sub-blocks
     const unsigned long long warps = (unsigned long long)p->grid * (p->block / 32);
-    int batch = p->launch.batch > 0 ? (p->launch.batch + kUnit - 1) / kUnit * kUnit : 0;
+    int batch = p->launch.batch > 0 ? (int)((p->launch.batch + kUnit - 1) / kUnit * kUnit) : 0;
     if (batch == 0) {
         unsigned long long b = span / (warps * 8);
         b = (b + kUnit - 1) / kUnit * kUnit;
-        batch = (int)std::min<unsigned long long>(std::max<unsigned long long>(b, kUnit), 4 * kUnit);
+        batch = (int)std::min<unsigned long long>(std::max<unsigned long long>(b, kUnit),
+                                                  std::max<unsigned long long>(4 * kUnit, 4096));
     }
     p->batch = batch;
     p->last_lo = lo;
