@@ -68,7 +68,9 @@ typedef struct pms_launch {
     int32_t algo;            /* PMS_ALGO_*: which kernel family (0 = auto)   */
     int32_t block_digits;    /* PMS_ALGO_BLOCK suffix digits S (5: 1024-, 6:
                                 4096-candidate blocks); 0 = auto (6 if l >= 13)*/
-    int32_t reserved[3];
+    int32_t table_global;    /* 1 = read the packed table from global memory
+                                (L1/L2) instead of staging it in smem        */
+    int32_t reserved[2];
 } pms_launch;
 
 /* Kernel families (pms_launch.algo).  Every family returns the same set.

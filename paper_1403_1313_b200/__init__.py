@@ -37,7 +37,8 @@ class Launch(ctypes.Structure):
                 ("batch", ctypes.c_int32), ("lanes_per_cand", ctypes.c_int32),
                 ("force_generic", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
                 ("no_skip", ctypes.c_int32), ("algo", ctypes.c_int32),
-                ("block_digits", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("block_digits", ctypes.c_int32), ("table_global", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class Stats(ctypes.Structure):

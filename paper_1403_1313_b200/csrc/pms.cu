@@ -684,7 +684,13 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     const uint32_t static_smem = 12288;  // mbarrier, per-warp hit masks, slack
     const uint32_t ball_bytes =
         block_algo ? (uint32_t)(S == 6 ? BlkTraits<6>::TWORDS : BlkTraits<5>::TWORDS) * 4u : 0u;
-    p->in_smem = p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
+    p->in_smem = !p->launch.table_global &&
+                 p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
+    // block family: a table that leaves room for only one CTA per SM is read
+    // through L1/L2 instead -- two resident CTAs win (measured at (16,5):
+    // 8.6 ms vs 9.9 ms); 228 KB of shared memory per SM, 1 KB reserved per CTA
+    if (block_algo && p->in_smem && 2u * (p->tab_bytes + ball_bytes + static_smem + 1024u) > 233472u)
+        p->in_smem = 0;
     p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0);
 
     RegKernel rk{};

@@ -27,14 +27,17 @@ def main():
     ap.add_argument("--ctas", type=int, nargs="+", default=[0])
     ap.add_argument("--batch", type=int, nargs="+", default=[0])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--S", type=int, nargs="+", default=[0])
+    ap.add_argument("--tglobal", type=int, nargs="+", default=[0])
     args = ap.parse_args()
     c = fmgen.BASELINE_CONFIGS[args.cfg]
     s, _ = fmgen.generate_fm(c["n"], c["t"], c["l"], c["d"], args.seed)
     algo = pms.ALGO_BLOCK if args.algo == "block" else pms.ALGO_CANDIDATE
     ref = None
     rows = []
-    for w, ct, b in itertools.product(args.warps, args.ctas, args.batch):
-        L = pms.Launch(algo=algo, warps_per_cta=w, ctas_per_sm=ct, batch=b)
+    for w, ct, b, S, tg in itertools.product(args.warps, args.ctas, args.batch, args.S, args.tglobal):
+        L = pms.Launch(algo=algo, warps_per_cta=w, ctas_per_sm=ct, batch=b, block_digits=S,
+                       table_global=tg)
         best = None
         for _ in range(args.reps):
             r = pms.find_ex(s, c["l"], c["d"], launch=L, max_out=1 << 22)
@@ -43,7 +46,8 @@ def main():
                 ref = r.codes.tolist()
             assert r.codes.tolist() == ref
             best = r.stats.search_ms if best is None else min(best, r.stats.search_ms)
-        row = dict(warps=w, ctas_per_sm=ct, batch=b, grid=r.stats.grid, block=r.stats.block,
+        row = dict(warps=w, ctas_per_sm=ct, batch=b, S=r.stats.block_digits, tglobal=tg,
+                   grid=r.stats.grid, block=r.stats.block,
                    nw=r.stats.windows_per_lane, search_ms=best,
                    cands_per_s=(4 ** c["l"]) / (best * 1e-3),
                    issued_per_s=r.stats.issued_compares / (best * 1e-3),
