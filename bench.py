@@ -278,6 +278,26 @@ def run_gpu(args) -> int:
                 "kernel": {"grid": cst.grid, "block": cst.block, "lanes_per_cand": cst.lanes_per_cand,
                            "windows_per_lane": cst.windows_per_lane}}
 
+    # ------------- block-family R_mix: the same kernel and mix without early exits
+    rmix_block = None
+    if last.algo == pms.ALGO_BLOCK and args.rmix_steps > 0:
+        with pms.Plan(n, t, l, d, pms.Launch(algo=pms.ALGO_BLOCK, no_skip=1,
+                                             block_digits=last.block_digits)) as rplan:
+            rms, rissued = [], 0
+            with torch.cuda.stream(stream):
+                for i in range(1 + args.rmix_steps):
+                    rplan.execute_tensors(seqs, out, cnt, 0, total, stream=stream)
+                    status, rst = rplan.wait()
+                    assert status == 0
+                    if i:
+                        rms.append(rst.search_ms)
+                        rissued += rst.issued_compares
+        rmix_block = {"window_tests_per_s": rissued / args.rmix_steps / (np.mean(rms) * 1e-3),
+                      "search_kernel_ms": float(np.mean(rms)),
+                      "basis": "block kernel with the skip rule off (pms_launch.no_skip): every "
+                               "block scans all n sequences -- the same scan + hit-resolution "
+                               "instruction mix with no early exit, all SMs"}
+
     # ------------------------------------------------ roofline microbenchmark
     with ClockSampler(dev.index) as clk_rm:
         rm = pms.roofline(1 << 15)
@@ -360,9 +380,15 @@ def run_gpu(args) -> int:
                      "peak_basis": f"POPC {POPC_PER_CLK_SM}/clk/SM x {sms} SMs x {sm_mhz:.0f} MHz "
                                    "(median SM clock in the timed region; one POPC per test)",
                      "achieved_basis": basis,
-                     "r_mix": rm["compares_per_s"] / 1e9,
-                     "r_mix_basis": "pms_roofline: the candidate kernel's per-compare loop, "
+                     "r_mix": (rmix_block["window_tests_per_s"] if rmix_block
+                               else rm["compares_per_s"]) / 1e9,
+                     "frac_of_r_mix": (achieved / (rmix_block["window_tests_per_s"] if rmix_block
+                                                   else rm["compares_per_s"])) if achieved else None,
+                     "r_mix_basis": rmix_block["basis"] if rmix_block else
+                                    "pms_roofline: the candidate kernel's per-compare loop, "
                                     "register-resident, no early exit, all SMs",
+                     "r_mix_kernel_ms": rmix_block["search_kernel_ms"] if rmix_block else None,
+                     "r_mix_candidate_loop": rm["compares_per_s"] / 1e9,
                      "r_mix_clocks": clk_rm.summary()},
         "candidate_kernel": cand,
         "cpu_baseline": cpu,
@@ -388,6 +414,8 @@ def main() -> int:
     ap.add_argument("--candidate-steps", type=int, default=3,
                     help="also time the per-candidate kernel for this many steps")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--rmix-steps", type=int, default=3,
+                    help="steps of the block kernel without early exit (block-family R_mix)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=5.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

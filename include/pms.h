@@ -63,8 +63,10 @@ typedef struct pms_launch {
     int32_t grid_ctas;       /* total persistent CTAs (overrides ctas_per_sm;
                                 the "workers" of the paper's Fig. 3/4 sweep)  */
     int32_t no_skip;         /* 1 = plain brute force (PAPER.md:63 before the
-                                "enhanced version"): every candidate scans all
-                                n sequences; same result, n*W compares each  */
+                                "enhanced version"): every candidate (block
+                                family: every block) scans all n sequences;
+                                same result.  With algo = AUTO this runs the
+                                candidate family (n*W compares per candidate)*/
     int32_t algo;            /* PMS_ALGO_*: which kernel family (0 = auto)   */
     int32_t block_digits;    /* PMS_ALGO_BLOCK suffix digits S (5: 1024-, 6:
                                 4096-candidate blocks); 0 = auto (6 if l >= 13)*/

@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
             int i = 0;
             bool dead = false;
             for (; i < a.n; ++i) {
-                if (i > 0) {
+                if (i > 0 && a.skip) {
                     int na = 0;
 #pragma unroll
                     for (int k = 0; k < B::KW; ++k) na += __popc(alive[k]);
@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
                 ++bscans;
                 if (!__any_sync(kFull, any != 0u)) {  // skip rule for the whole block
                     dead = true;
-                    break;
+                    if (a.skip) break;  // (a.skip == 0: plain brute force scans on)
                 }
             }
             if (dead) continue;
@@ -660,8 +660,11 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         destroy_plan(p);
         return fail_cuda(__LINE__);
     }
-    const bool block_algo = (p->launch.algo == PMS_ALGO_BLOCK || p->launch.algo == PMS_ALGO_AUTO) &&
-                            !p->launch.no_skip && l >= kBlkMinL;
+    // block family: AUTO or explicit; with no_skip only when asked for explicitly
+    // (AUTO + no_skip keeps the per-candidate plain brute force)
+    const bool block_algo =
+        (p->launch.algo == PMS_ALGO_BLOCK || (p->launch.algo == PMS_ALGO_AUTO && !p->launch.no_skip)) &&
+        l >= kBlkMinL;
     // block digits S: 6 (4096-candidate blocks) when there are enough blocks to
     // keep every warp busy (l >= 13: >= 16k blocks), else 5
     int S = p->launch.block_digits == 5 || p->launch.block_digits == 6 ? p->launch.block_digits

@@ -415,3 +415,18 @@ def test_pooled_plans_sharing_a_kernel(orc):
         assert r1.status == r2.status == r3.status == 0, pms.last_error()
         assert r1.codes.tolist() == r3.codes.tolist() == orc.find(big, 7, 2).codes.tolist()
         assert r2.codes.tolist() == orc.find(small, 7, 2).codes.tolist()
+
+
+def test_block_algo_without_skip_rule(orc):
+    """algo = BLOCK + no_skip: every block scans all n sequences (plain brute
+    force, bit-parallel over 4^S candidates); same set; (block, sequence)
+    scans = blocks * n exactly."""
+    for S in (5, 6):
+        L = pms.Launch(algo=pms.ALGO_BLOCK, block_digits=S, no_skip=1)
+        s, _ = fmgen.generate_fm(6, 100, 9, 2, S)
+        got, _ = assert_same(s, 9, 2, orc, launch=L)
+        assert got.stats.block_scans == (4 ** 9 // 4 ** S) * 6
+        assert got.stats.issued_compares == got.stats.block_scans * 92
+        for seed in range(3):
+            s = fmgen.random_sequences(3, 40, 80 + seed)
+            assert_same(s, 7, 2, orc, launch=L)
