@@ -186,6 +186,11 @@ const char *pms_strerror(int status);
  * line and CUDA error string); "" if none.  Owned by the library. */
 const char *pms_last_error(void);
 
+/* Debug builds (libpms_b200_debug.so, -DPMS_DEBUG_CHECKS) count out-of-range
+ * device indices instead of accessing them; returns the count (reset to 0 if
+ * `reset`), -1 in release builds, -2 on a device error. */
+int64_t pms_debug_violations(int32_t reset);
+
 /* Number of SMs and the opt-in shared memory per block of the current
  * device (for reporting); PMS_E_CUDA without a device. */
 int pms_device_info(int32_t *sms, int32_t *smem_optin_bytes,

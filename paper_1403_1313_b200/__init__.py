@@ -90,6 +90,8 @@ def load() -> ctypes.CDLL:
         lib.pms_roofline.restype = ctypes.c_int
         lib.pms_strerror.argtypes = [ctypes.c_int]
         lib.pms_strerror.restype = ctypes.c_char_p
+        lib.pms_debug_violations.argtypes = [ctypes.c_int32]
+        lib.pms_debug_violations.restype = ctypes.c_int64
         lib.pms_last_error.argtypes = []
         lib.pms_last_error.restype = ctypes.c_char_p
         lib.pms_device_info.argtypes = [ctypes.POINTER(i32)] * 3
@@ -100,6 +102,11 @@ def load() -> ctypes.CDLL:
 
 def strerror(status: int) -> str:
     return load().pms_strerror(int(status)).decode()
+
+
+def debug_violations(reset: bool = False) -> int:
+    """Out-of-range device indices counted by the debug build (-1: release)."""
+    return int(load().pms_debug_violations(1 if reset else 0))
 
 
 def last_error() -> str:

@@ -83,6 +83,7 @@ __global__ void pms_pack_kernel(const uint8_t* __restrict__ seqs, int n, int t, 
     const int k = (int)(idx - (long long)i * Wp);
     const uint8_t* p = seqs + (long long)i * t + min(k, W - 1);
     uint32_t H = 0, L = 0, bad = 0;
+    PMS_CHECK(min(k, W - 1) + l <= t);
     for (int j = 0; j < l; ++j) {
         const uint32_t u = p[j] & 0xDFu;  // upper-case; only 'x'/'X' map to 'X'
         const uint32_t code = u == 'A' ? 0u : u == 'C' ? 1u : u == 'G' ? 2u : u == 'T' ? 3u : 4u;
@@ -125,6 +126,7 @@ __device__ __forceinline__ bool check_sequences(const uint32_t* tab, int i0, int
         uint32_t m = 0xFFu;
 #pragma unroll 4
         for (int k = lane; k < Wp; k += 32) {
+            PMS_CHECK(i < n && k < Wp);
             const uint32_t w = row[k];
             m = min(m, mism2(cb, cr, w, rot16(w)));
         }
@@ -303,21 +305,24 @@ __device__ __forceinline__ uint32_t sfx_code(uint32_t h, uint32_t l) {
 // Process every pending hit of every lane (hm bits index the lane's windows
 // row[lane + 32*j]) and OR the matching candidates into the lane's acc words.
 template <int S>
-__device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uint32_t cb,
+__device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, int wp, uint32_t cb,
                                            uint32_t d2, int lane, const uint32_t* T,
                                            uint32_t* wmask,
                                            uint32_t (&acc)[BlkTraits<S>::KW]) {
+    (void)wp;  // row length (windows), used by the debug bounds checks
     using B = BlkTraits<S>;
     while (__any_sync(kFull, hm != 0u)) {
         uint32_t mine = kFull;
         if (hm) {
             const int j = __ffs(hm) - 1;
             hm &= hm - 1;
+            PMS_CHECK(lane + 32 * j < wp);
             const uint32_t w = row[lane + 32 * j];
             const uint32_t x = (cb ^ w) & ~B::SFX;
             const uint32_t p2 = __popc(x | rot16(x));
             const uint32_t eH = (w >> 16) & B::M, eL = w & B::M;
             if (p2 == d2) {
+                PMS_CHECK(((eH << B::X) | (eL >> 5)) < 32u * B::KW);
                 atomicOr(&wmask[(eH << B::X) | (eL >> 5)], 1u << (eL & 31u));
             } else {  // record: (r-1) row, eL & 31, eH in the low S bits, eL >> 5 on top
                 const uint32_t r = min((d2 - p2) >> 1, (uint32_t)S);
@@ -330,6 +335,7 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uin
             who &= who - 1;
             const uint32_t v = __shfl_sync(kFull, mine, src);
             if (B::X == 0) {
+                PMS_CHECK((v ^ (uint32_t)lane) < (uint32_t)B::TWORDS);
                 acc[0] |= T[v ^ (uint32_t)lane];
             } else {
                 const uint32_t vx = v & 0x00FFFFFFu, eLt = v >> 24;
@@ -337,6 +343,7 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const uint32_t* row, uin
                 for (int k = 0; k < B::KW; ++k) {
                     const uint32_t hk = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
                     const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
+                    PMS_CHECK(((vx ^ hk) | ((lt ^ eLt) << 5)) < (uint32_t)B::TWORDS);
                     acc[k] |= T[(vx ^ hk) | ((lt ^ eLt) << 5)];
                 }
             }
@@ -444,21 +451,23 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
                     } else {
 #pragma unroll
                         for (int j = 0; j < NW; ++j) {
+                            PMS_CHECK(lane + 32 * j < a.Wp && i < a.n);
                             const uint32_t x = (cb ^ row[lane + 32 * j]) & ~B::SFX;
                             if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
                         }
                     }
                     // pass 2: resolve the hits into each lane's candidate words
-                    drain_hits<S>(hm, row, cb, a.d2, lane, T, wmask, acc);
+                    drain_hits<S>(hm, row, a.Wp, cb, a.d2, lane, T, wmask, acc);
                 } else {
                     for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
                         uint32_t hm = 0;
                         const int nj = min(a.Wp - k0, 32 * 32) / 32;
                         for (int j = 0; j < nj; ++j) {
+                            PMS_CHECK(k0 + lane + 32 * j < a.Wp && i < a.n);
                             const uint32_t x = (cb ^ row[k0 + lane + 32 * j]) & ~B::SFX;
                             if (__popc(x | rot16(x)) <= a.d2) hm |= 1u << j;
                         }
-                        drain_hits<S>(hm, row + k0, cb, a.d2, lane, T, wmask, acc);
+                        drain_hits<S>(hm, row + k0, a.Wp - k0, cb, a.d2, lane, T, wmask, acc);
                     }
                 }
                 uint32_t any = 0;
@@ -1088,6 +1097,22 @@ extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compa
 }
 
 extern "C" const char* pms_last_error(void) { return g_last_error; }
+
+extern "C" int64_t pms_debug_violations(int32_t reset) {
+#ifdef PMS_DEBUG_CHECKS
+    if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+    unsigned int v = 0;
+    if (cudaMemcpyFromSymbol(&v, pms::g_pms_violations, sizeof(v)) != cudaSuccess) return -2;
+    if (reset) {
+        const unsigned int z = 0;
+        cudaMemcpyToSymbol(pms::g_pms_violations, &z, sizeof(z));
+    }
+    return (int64_t)v;
+#else
+    (void)reset;
+    return -1;
+#endif
+}
 
 extern "C" const char* pms_strerror(int status) {
     switch (status) {

@@ -18,6 +18,22 @@
 
 namespace pms {
 
+// Debug builds (-DPMS_DEBUG_CHECKS, libpms_b200_debug.so) count every
+// out-of-range index instead of performing the access's check silently; the
+// host reads the counter with pms_debug_violations().  No trap, so a bad index
+// cannot fault the device.  Release builds compile the checks away.
+#ifdef PMS_DEBUG_CHECKS
+__device__ unsigned int g_pms_violations;
+#define PMS_CHECK(cond)                                          \
+    do {                                                         \
+        if (!(cond)) atomicAdd(&::pms::g_pms_violations, 1u);    \
+    } while (0)
+#else
+#define PMS_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 struct DevState {
     unsigned long long next;    // work counter: candidates handed out, from lo_al
     unsigned long long extra;   // sequences scanned beyond sequence 0 (survivors)

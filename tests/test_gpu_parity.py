@@ -29,6 +29,12 @@ def _gpu():
         pytest.fail("no CUDA device: GPU tests must run on the B200 box")
     pms.build()
     pms.load()
+    debug = os.environ.get("PMS_DEBUG_LIB") == "1"
+    if debug:
+        pms.debug_violations(reset=True)
+    yield
+    if debug:  # bounds-checked build: no out-of-range device index anywhere
+        assert pms.debug_violations() == 0
 
 
 CAND = pms.Launch(algo=pms.ALGO_CANDIDATE)
