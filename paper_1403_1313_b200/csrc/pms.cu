@@ -889,6 +889,9 @@ struct CallCtx {
     unsigned long long out_cap = 0;
     uint64_t* d_count = nullptr;
     uint64_t* h_count = nullptr;  // pinned
+    uint8_t* h_seqs = nullptr;    // pinned staging of the input (n*t bytes)
+    uint32_t* h_out = nullptr;    // pinned staging of small result sets
+    static constexpr unsigned long long kHostOutCap = 1ull << 16;
     cudaStream_t stream = nullptr;
 
     bool matches(int dv, int32_t n_, int32_t t_, int32_t l_, int32_t d_,
@@ -902,6 +905,8 @@ struct CallCtx {
         cudaFree(d_out);
         cudaFree(d_count);
         cudaFreeHost(h_count);
+        cudaFreeHost(h_seqs);
+        cudaFreeHost(h_out);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -939,6 +944,8 @@ int ctx_acquire(int32_t n, int32_t t, int32_t l, int32_t d, const pms_launch& L,
     if (cudaMalloc(&c->d_seqs, (size_t)n * t) != cudaSuccess ||
         cudaMalloc(&c->d_count, sizeof(uint64_t)) != cudaSuccess ||
         cudaMallocHost(&c->h_count, sizeof(uint64_t)) != cudaSuccess ||
+        cudaMallocHost(&c->h_seqs, (size_t)n * t) != cudaSuccess ||
+        cudaMallocHost(&c->h_out, CallCtx::kHostOutCap * sizeof(uint32_t)) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
         ctx_destroy(c);
         return fail_cuda(__LINE__);
@@ -996,7 +1003,9 @@ extern "C" int pms_find_ex(const uint8_t* seqs, int32_t n, int32_t t, int32_t l,
         c->out_cap = cap;
     }
     cudaStream_t s = c->stream;
-    if (cudaMemcpyAsync(c->d_seqs, seqs, (size_t)n * t, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    std::memcpy(c->h_seqs, seqs, (size_t)n * t);  // pinned staging: the H2D is a true async DMA
+    if (cudaMemcpyAsync(c->d_seqs, c->h_seqs, (size_t)n * t, cudaMemcpyHostToDevice, s) !=
+        cudaSuccess) {
         healthy = false;
         return fail_cuda(__LINE__);
     }
@@ -1023,12 +1032,14 @@ extern "C" int pms_find_ex(const uint8_t* seqs, int32_t n, int32_t t, int32_t l,
     if (found > max_out) return PMS_E_TRUNCATED;
     // a7: D2H of the codes, host sort (ascending code = lexicographic order)
     if (found > 0) {
-        if (cudaMemcpyAsync(out_codes, c->d_out, found * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                            s) != cudaSuccess ||
+        const bool staged = found <= CallCtx::kHostOutCap;
+        if (cudaMemcpyAsync(staged ? c->h_out : out_codes, c->d_out, found * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s) != cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess) {
             healthy = false;
             return fail_cuda(__LINE__);
         }
+        if (staged) std::memcpy(out_codes, c->h_out, found * sizeof(uint32_t));
         std::sort(out_codes, out_codes + found);
     }
     return PMS_OK;
