@@ -138,7 +138,7 @@ def find_ex(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
     n, t = a.shape
     if hi is None:
         hi = (1 << 64) - 1
-    out = np.zeros(max(int(max_out), 1), dtype=np.uint32)
+    out = np.empty(max(int(max_out), 1), dtype=np.uint32)
     cnt = ctypes.c_uint64(0)
     st = Stats() if want_stats else None
     status = lib.pms_find_ex(a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), n, t, l, d,
