@@ -186,7 +186,10 @@ def run_gpu(args) -> int:
     pms.load()
 
     n, t, l, d = WORKLOAD["n"], WORKLOAD["t"], WORKLOAD["l"], WORKLOAD["d"]
-    seed = args.seed + rank
+    strong = args.scaling == "strong"
+    # weak: one independent instance per rank; strong: one instance, the candidate
+    # range split over the ranks (shard.shard_range) and gathered every step
+    seed = args.seed if strong else args.seed + rank
     seqs_np, rec = fmgen.generate_fm(n, t, l, d, seed)
     seqs = torch.from_numpy(seqs_np).to(dev)
     cap = 1 << 20
@@ -197,9 +200,19 @@ def run_gpu(args) -> int:
     algo = {"auto": pms.ALGO_AUTO, "candidate": pms.ALGO_CANDIDATE, "block": pms.ALGO_BLOCK}[args.algo]
     plan = pms.Plan(n, t, l, d, pms.Launch(algo=algo))
     total = 4 ** l
+    from paper_1403_1313_b200.shard import shard_range
+    lo, hi = shard_range(total, rank, world) if strong else (0, total)
+    gbuf = torch.zeros(64, dtype=torch.int64, device=dev)
 
     def step(ev_end=None):
-        plan.execute_tensors(seqs, out, cnt, 0, total, stream=stream)
+        plan.execute_tensors(seqs, out, cnt, lo, hi, stream=stream)
+        if strong and dist:  # the exchange step: gather every rank's count and codes
+            cl = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+            dist.all_gather(cl, cnt)
+            gbuf[:] = -1
+            gbuf[:64].copy_(out[:64].to(torch.int64))
+            gl = [torch.zeros(64, dtype=torch.int64, device=dev) for _ in range(world)]
+            dist.all_gather(gl, gbuf)
         if ev_end is not None:  # end of the step's device work, before the host waits
             ev_end.record(stream)
         status, st = plan.wait()
@@ -239,6 +252,10 @@ def run_gpu(args) -> int:
         tmax = float(x.item())
     nfound = int(cnt.item())
     codes = sorted(out[:nfound].cpu().numpy().astype(np.uint32).tolist())
+    if strong and dist:  # the full set = union of the rank shards (in range order)
+        from paper_1403_1313_b200.shard import gather_codes
+        codes = sorted(gather_codes(np.asarray(codes, dtype=np.uint32), device=dev).tolist())
+        nfound = len(codes)
     c_alg, gold = golden_c_alg(seed)
     parity = None if gold is None else (codes == gold)
 
@@ -246,7 +263,7 @@ def run_gpu(args) -> int:
     e2e_ms = []
     for i in range(args.warmup + args.e2e_steps):
         t0 = time.perf_counter()
-        r = pms.find_ex(seqs_np, l, d, launch=pms.Launch(algo=algo), max_out=cap,
+        r = pms.find_ex(seqs_np, l, d, lo=lo, hi=hi, launch=pms.Launch(algo=algo), max_out=cap,
                         want_stats=False)
         dt = time.perf_counter() - t0
         assert r.status == 0
@@ -309,7 +326,7 @@ def run_gpu(args) -> int:
         return 0
 
     search_avg = float(np.mean(search_ms))
-    cands_per_s = world * args.steps * total / (tmax * 1e-3)
+    cands_per_s = (1 if strong else world) * args.steps * total / (tmax * 1e-3)
     sm_mhz = cs["sm_mhz"] or 1965.0
     sms = pms.device_info()["sms"]
     peak_popc = POPC_PER_CLK_SM * sms * sm_mhz * 1e6
@@ -355,11 +372,14 @@ def run_gpu(args) -> int:
     line = {
         "metric": METRIC, "value": cands_per_s, "unit": "candidates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmax / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
         "config": {"workload": WORKLOAD["name"] + " FM (BASELINE.json configs[3])",
                    "n": n, "t": t, "l": l, "d": d,
-                   "seeds": [args.seed + r for r in range(world)],
+                   "seeds": [args.seed] if strong else [args.seed + r for r in range(world)],
+                   "sharding": ("candidate-code range split over ranks, counts+codes "
+                                "all_gather per step" if strong else
+                                "one independent instance per rank, no collective"),
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
                    "algo": {1: "candidate", 2: "block"}.get(last.algo, str(last.algo)),
                    "kernel": {"grid": last.grid, "block": last.block,
@@ -367,7 +387,8 @@ def run_gpu(args) -> int:
                               "windows_per_lane": last.windows_per_lane,
                               "table_in_smem": last.table_in_smem,
                               "smem_bytes": last.smem_bytes}},
-        "window_compares_per_s": (world * c_alg / (tmax * 1e-3 / args.steps)) if c_alg else None,
+        "window_compares_per_s": ((1 if strong else world) * c_alg / (tmax * 1e-3 / args.steps))
+        if c_alg else None,
         "window_compares_basis": "oracle C_alg (candidate-window tests of skip-BF with "
                                  "first-match stop) per step / device time per step",
         "issued_window_tests_per_s": issued_rate,
@@ -393,7 +414,7 @@ def run_gpu(args) -> int:
                      "r_mix_clocks": clk_rm.summary()},
         "candidate_kernel": cand,
         "cpu_baseline": cpu,
-        "e2e": {"value": world * args.e2e_steps * total / (e2e_tot * 1e-3),
+        "e2e": {"value": (1 if strong else world) * args.e2e_steps * total / (e2e_tot * 1e-3),
                 "unit": "candidates/s", "h2d_bytes_per_step": n * t,
                 "d2h_bytes_per_step": 8 + 4 * nfound + 32,
                 "path": "pms_find_ex from host buffers (pooled context, H2D, kernels, D2H, sort)"},
@@ -412,6 +433,8 @@ def main() -> int:
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--algo", choices=["auto", "candidate", "block"], default="auto")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: an instance per rank; strong: one instance sharded by candidate range")
     ap.add_argument("--candidate-steps", type=int, default=3,
                     help="also time the per-candidate kernel for this many steps")
     ap.add_argument("--e2e-steps", type=int, default=20)
