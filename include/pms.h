@@ -72,7 +72,10 @@ typedef struct pms_launch {
                                 4096-candidate blocks); 0 = auto (6 if l >= 13)*/
     int32_t table_global;    /* 1 = read the packed table from global memory
                                 (L1/L2) instead of staging it in smem        */
-    int32_t reserved[2];
+    int32_t handoff;         /* block family: a block with at most this many
+                                live candidates finishes them one by one
+                                (0 = auto)                                   */
+    int32_t reserved[1];
 } pms_launch;
 
 /* Kernel families (pms_launch.algo).  Every family returns the same set.

@@ -38,7 +38,7 @@ class Launch(ctypes.Structure):
                 ("force_generic", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
                 ("no_skip", ctypes.c_int32), ("algo", ctypes.c_int32),
                 ("block_digits", ctypes.c_int32), ("table_global", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("handoff", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class Stats(ctypes.Structure):

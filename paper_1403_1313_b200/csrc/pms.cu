@@ -62,6 +62,7 @@ struct SearchArgs {
     int batch;                      // candidates per atomic grab (multiple of kSub)
     int in_smem;                    // stage the table into shared memory (TMA bulk)
     int skip;                       // 1 = skip rule (skip-BF); 0 = plain brute force
+    int handoff;                    // block family: <= this many survivors -> per-candidate
     uint32_t tab_bytes;
     DevState* st;
     unsigned long long* nout;       // result counter (caller's d_count)
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
                     int na = 0;
 #pragma unroll
                     for (int k = 0; k < B::KW; ++k) na += __popc(alive[k]);
-                    if (__reduce_add_sync(kFull, na) <= 1) break;
+                    if (__reduce_add_sync(kFull, na) <= a.handoff) break;
                 }
                 const uint32_t* row = tab + (size_t)i * a.Wp;
                 uint32_t acc[B::KW];
@@ -496,21 +497,30 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
                 }
                 continue;
             }
-            // one survivor left: the whole warp finishes it from sequence i on
-            uint32_t pick = kFull;  // (k << 5) | bit of this lane's first alive candidate
+            // at most a.handoff survivors left: the whole warp finishes each one
+            // from sequence i on with the per-candidate check
+            for (;;) {
+                uint32_t pick = kFull;  // (k << 5) | bit of this lane's first alive candidate
 #pragma unroll
-            for (int k = B::KW - 1; k >= 0; --k)
-                if (alive[k]) pick = ((uint32_t)k << 5) | (__ffs(alive[k]) - 1);
-            const uint32_t holder = __ballot_sync(kFull, pick != kFull);
-            const int src = __ffs(holder) - 1;
-            const uint32_t pk = __shfl_sync(kFull, pick, src);
-            const uint32_t k = pk >> 5;
-            const uint32_t h = ((uint32_t)src << B::X) | (k >> B::X);
-            const uint32_t l5 = ((k & ((1u << B::X) - 1u)) << 5) | (pk & 31u);
-            const uint32_t code = (uint32_t)(cbase + sfx_code(h, l5));
-            if (check_sequences(tab, i, a.n, a.Wp, code_to_bp(code), a.d2, lane, scanned) &&
-                lane == 0)
-                append(a, code);
+                for (int k = B::KW - 1; k >= 0; --k)
+                    if (alive[k]) pick = ((uint32_t)k << 5) | (__ffs(alive[k]) - 1);
+                const uint32_t holder = __ballot_sync(kFull, pick != kFull);
+                if (!holder) break;
+                const int src = __ffs(holder) - 1;
+                const uint32_t pk = __shfl_sync(kFull, pick, src);
+                const uint32_t k = pk >> 5;
+                if (lane == src) {
+#pragma unroll
+                    for (int q = 0; q < B::KW; ++q)
+                        if (q == (int)k) alive[q] &= alive[q] - 1;  // clear the picked bit
+                }
+                const uint32_t h = ((uint32_t)src << B::X) | (k >> B::X);
+                const uint32_t l5 = ((k & ((1u << B::X) - 1u)) << 5) | (pk & 31u);
+                const uint32_t code = (uint32_t)(cbase + sfx_code(h, l5));
+                if (check_sequences(tab, i, a.n, a.Wp, code_to_bp(code), a.d2, lane, scanned) &&
+                    lane == 0)
+                    append(a, code);
+            }
         }
     }
     if (lane == 0) {
@@ -807,6 +817,7 @@ extern "C" int pms_plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo,
     a.lo = lo; a.hi = hi; a.lo_al = lo_al; a.span = span; a.batch = batch;
     a.in_smem = p->in_smem; a.tab_bytes = p->tab_bytes;
     a.skip = p->launch.no_skip ? 0 : 1;
+    a.handoff = p->launch.handoff > 0 ? p->launch.handoff : (p->d >= 5 ? 3 : 1);  // measured
     a.st = p->d_state; a.nout = reinterpret_cast<unsigned long long*>(d_count);
     a.out = d_out; a.cap = cap;
 

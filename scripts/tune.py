@@ -29,15 +29,17 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--S", type=int, nargs="+", default=[0])
     ap.add_argument("--tglobal", type=int, nargs="+", default=[0])
+    ap.add_argument("--handoff", type=int, nargs="+", default=[0])
     args = ap.parse_args()
     c = fmgen.BASELINE_CONFIGS[args.cfg]
     s, _ = fmgen.generate_fm(c["n"], c["t"], c["l"], c["d"], args.seed)
     algo = pms.ALGO_BLOCK if args.algo == "block" else pms.ALGO_CANDIDATE
     ref = None
     rows = []
-    for w, ct, b, S, tg in itertools.product(args.warps, args.ctas, args.batch, args.S, args.tglobal):
+    for w, ct, b, S, tg, ho in itertools.product(args.warps, args.ctas, args.batch, args.S,
+                                                 args.tglobal, args.handoff):
         L = pms.Launch(algo=algo, warps_per_cta=w, ctas_per_sm=ct, batch=b, block_digits=S,
-                       table_global=tg)
+                       table_global=tg, handoff=ho)
         best = None
         for _ in range(args.reps):
             r = pms.find_ex(s, c["l"], c["d"], launch=L, max_out=1 << 22)
@@ -46,7 +48,7 @@ def main():
                 ref = r.codes.tolist()
             assert r.codes.tolist() == ref
             best = r.stats.search_ms if best is None else min(best, r.stats.search_ms)
-        row = dict(warps=w, ctas_per_sm=ct, batch=b, S=r.stats.block_digits, tglobal=tg,
+        row = dict(warps=w, ctas_per_sm=ct, batch=b, S=r.stats.block_digits, tglobal=tg, handoff=ho,
                    grid=r.stats.grid, block=r.stats.block,
                    nw=r.stats.windows_per_lane, search_ms=best,
                    cands_per_s=(4 ** c["l"]) / (best * 1e-3),

@@ -436,3 +436,14 @@ def test_block_algo_without_skip_rule(orc):
         for seed in range(3):
             s = fmgen.random_sequences(3, 40, 80 + seed)
             assert_same(s, 7, 2, orc, launch=L)
+
+
+def test_block_algo_handoff_thresholds(orc):
+    """Any hand-off threshold (block scans -> per-candidate checks) gives the
+    same set, including several survivors finished one by one."""
+    s, _ = fmgen.generate_fm(12, 150, 9, 2, 21)
+    want = orc.find(s, 9, 2).codes.tolist()
+    for S in (5, 6):
+        for h in (1, 2, 5, 40, 5000):
+            L = pms.Launch(algo=pms.ALGO_BLOCK, block_digits=S, handoff=h)
+            assert gpu(s, 9, 2, launch=L).codes.tolist() == want, (S, h)
