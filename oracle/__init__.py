@@ -54,6 +54,9 @@ def _load():
             f = getattr(lib, name)
             f.argtypes = [u8p, i32, i32, i32, i32, u64, u64, i32, u32p, u64, u64p, u64p]
             f.restype = ctypes.c_int
+        lib.oracle_find64.argtypes = [u8p, i32, i32, i32, i32, u64, u64, i32, u64p, u64, u64p,
+                                      u64p]
+        lib.oracle_find64.restype = ctypes.c_int
         lib.oracle_ball_find.argtypes = [u8p, i32, i32, i32, i32, u32p, u64, u64p]
         lib.oracle_ball_find.restype = ctypes.c_int
         lib.oracle_verify_motif.argtypes = [u8p, i32, i32, i32, i32, u64]
@@ -113,6 +116,25 @@ def find(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
     over `threads` workers.  Returns every rank whose l-mer has a
     <= d mismatch window in all n sequences, ascending."""
     return _call("oracle_find", seqs, l, d, lo, hi, threads, max_out)
+
+
+def find64(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
+           threads: int | None = None, max_out: int = 1 << 22) -> OracleResult:
+    """Skip-BF for l <= 31 with 64-bit codes; same algorithm as
+    find().  Use [lo, hi) ranges: 4^l candidates are far too many for a CPU
+    at large l."""
+    lib = _load()
+    a, n, t = _as_rows(seqs)
+    if hi is None:
+        hi = 4 ** l if 1 <= l <= 31 else 0
+    out = np.empty(max(int(max_out), 1), dtype=np.uint64)
+    cnt, work = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    st = lib.oracle_find64(a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), n, t, l, d, lo, hi,
+                           threads if threads else default_threads(),
+                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), int(max_out),
+                           ctypes.byref(cnt), ctypes.byref(work))
+    k = min(int(cnt.value), int(max_out)) if st in (OK, E_TRUNCATED) else 0
+    return OracleResult(st, out[:k].copy(), int(cnt.value), int(work.value))
 
 
 def naive_find(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,

@@ -35,7 +35,8 @@ enum {
     ORC_E_NOMEM = -6
 };
 
-#define ORC_MAX_L 16
+#define ORC_MAX_L 31      /* oracle_find64 / verify (u64 codes) */
+#define ORC_MAX_L32 16    /* oracle_find / naive / ball (u32 codes, include/pms.h) */
 
 static const char ORC_ALPHABET[4] = {'A', 'C', 'G', 'T'}; /* A0 C1 G2 T3 */
 
@@ -74,12 +75,12 @@ int32_t oracle_hamming(const char *a, const char *b, int32_t l)
 /* Argument checks of include/pms.h, in the documented order (ARG, then
  * CHAR).  On success writes the upper-cased copy of seqs into norm. */
 static int orc_validate(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
-                        int32_t d, const uint32_t *out, uint64_t max_out,
-                        const uint64_t *count, char *norm)
+                        int32_t d, const void *out, uint64_t max_out,
+                        const uint64_t *count, char *norm, int32_t max_l)
 {
     if (seqs == NULL || count == NULL) return ORC_E_ARG;
     if (out == NULL && max_out > 0) return ORC_E_ARG;
-    if (n < 1 || t < 1 || l < 1 || l > ORC_MAX_L) return ORC_E_ARG;
+    if (n < 1 || t < 1 || l < 1 || l > max_l) return ORC_E_ARG;
     if (l > t) return ORC_E_ARG;   /* S:80 MotifLongerThanSequence */
     if (d < 0) return ORC_E_ARG;
     for (int64_t p = 0; p < (int64_t)n * t; ++p) {
@@ -98,7 +99,7 @@ typedef struct {
     const char *s;        /* upper-cased sequences, n rows of t chars */
     int32_t n, t, l, d;
     uint64_t lo, hi;      /* this worker's half-open rank range */
-    uint32_t *found;      /* ranks of motifs in this range, ascending */
+    uint64_t *found;      /* ranks of motifs in this range, ascending */
     uint64_t nfound, cap;
     uint64_t c_alg;       /* windows compared, first-match stop */
     int status;
@@ -130,12 +131,12 @@ static int orc_push(orc_job *jb, uint64_t r)
 {
     if (jb->nfound == jb->cap) {
         uint64_t nc = jb->cap ? 2 * jb->cap : 1024;
-        uint32_t *p = (uint32_t *)realloc(jb->found, nc * sizeof(uint32_t));
+        uint64_t *p = (uint64_t *)realloc(jb->found, nc * sizeof(uint64_t));
         if (!p) return ORC_E_NOMEM;
         jb->found = p;
         jb->cap = nc;
     }
-    jb->found[jb->nfound++] = (uint32_t)r;
+    jb->found[jb->nfound++] = r;
     return ORC_OK;
 }
 
@@ -209,12 +210,13 @@ void oracle_partition(uint64_t lo, uint64_t hi, int32_t workers,
  * already ascending. */
 static int orc_run(void *(*worker)(void *), const uint8_t *seqs, int32_t n,
                    int32_t t, int32_t l, int32_t d, uint64_t lo, uint64_t hi,
-                   int32_t threads, uint32_t *out, uint64_t max_out,
+                   int32_t threads, void *out, int wide, uint64_t max_out,
                    uint64_t *count, uint64_t *c_alg)
 {
     char *norm = (char *)malloc(seqs && n > 0 && t > 0 ? (size_t)n * t : 1);
     if (!norm) return ORC_E_NOMEM;
-    int st = orc_validate(seqs, n, t, l, d, out, max_out, count, norm);
+    int st = orc_validate(seqs, n, t, l, d, out, max_out, count, norm,
+                          wide ? ORC_MAX_L : ORC_MAX_L32);
     if (st != ORC_OK) { free(norm); return st; }
     uint64_t total = 1ull << (2 * l);
     if (hi > total) hi = total;
@@ -251,7 +253,10 @@ static int orc_run(void *(*worker)(void *), const uint8_t *seqs, int32_t n,
         uint64_t at = 0;
         for (int32_t w = 0; w < threads; ++w)
             for (uint64_t k = 0; k < jobs[w].nfound; ++k, ++at)
-                if (at < max_out) out[at] = jobs[w].found[k];
+                if (at < max_out) {
+                    if (wide) ((uint64_t *)out)[at] = jobs[w].found[k];
+                    else ((uint32_t *)out)[at] = (uint32_t)jobs[w].found[k];
+                }
         *count = nres;
         if (c_alg) *c_alg = work;
         if (nres > max_out) st = ORC_E_TRUNCATED;
@@ -271,7 +276,18 @@ int oracle_find(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
                 uint64_t *c_alg)
 {
     return orc_run(orc_skip_bf_worker, seqs, n, t, l, d, lo, hi, threads,
-                   out, max_out, count, c_alg);
+                   out, 0, max_out, count, c_alg);
+}
+
+/* The same skip-BF for l <= 31 with 64-bit codes (SPEC.md:117 caps l at 31 so
+ * a rank fits 64 bits). */
+int oracle_find64(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
+                  int32_t d, uint64_t lo, uint64_t hi, int32_t threads,
+                  uint64_t *out, uint64_t max_out, uint64_t *count,
+                  uint64_t *c_alg)
+{
+    return orc_run(orc_skip_bf_worker, seqs, n, t, l, d, lo, hi, threads,
+                   out, 1, max_out, count, c_alg);
 }
 
 /* Naive BF (no skip rule, no early abort) over [lo,hi); c_alg receives the
@@ -281,7 +297,7 @@ int oracle_naive_find(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
                       uint32_t *out, uint64_t max_out, uint64_t *count,
                       uint64_t *c_alg)
 {
-    return orc_run(orc_naive_worker, seqs, n, t, l, d, lo, hi, threads, out,
+    return orc_run(orc_naive_worker, seqs, n, t, l, d, lo, hi, threads, out, 0,
                    max_out, count, c_alg);
 }
 
@@ -330,7 +346,7 @@ int oracle_ball_find(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
     if (l > 12) return ORC_E_ARG; /* 4^12 = 16 MB bitmaps; tiny inputs only */
     char *norm = (char *)malloc(seqs && n > 0 && t > 0 ? (size_t)n * t : 1);
     if (!norm) return ORC_E_NOMEM;
-    int st = orc_validate(seqs, n, t, l, d, out, max_out, count, norm);
+    int st = orc_validate(seqs, n, t, l, d, out, max_out, count, norm, ORC_MAX_L32);
     if (st != ORC_OK) { free(norm); return st; }
     uint64_t total = 1ull << (2 * l);
     uint8_t *acc = (uint8_t *)malloc(total), *cur = (uint8_t *)malloc(total);
@@ -365,7 +381,7 @@ int oracle_verify_motif(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
     uint64_t dummy = 0;
     char *norm = (char *)malloc(seqs && n > 0 && t > 0 ? (size_t)n * t : 1);
     if (!norm) return ORC_E_NOMEM;
-    int st = orc_validate(seqs, n, t, l, d, NULL, 0, &dummy, norm);
+    int st = orc_validate(seqs, n, t, l, d, NULL, 0, &dummy, norm, ORC_MAX_L);
     if (st != ORC_OK) { free(norm); return st; }
     if (rank >= (1ull << (2 * l))) { free(norm); return ORC_E_ARG; }
     char m[ORC_MAX_L + 1];

@@ -343,3 +343,60 @@ def test_edge_shapes(orc):
     got = set(orc.find(s, 5, 1).codes.tolist())
     for c in range(4 ** 5):
         assert orc.verify_motif(s, 5, 1, c) == (c in got)
+
+
+# ----------------------------------------------------- l = 17..31 (u64 codes)
+
+def test_find64_matches_find_for_small_l(orc):
+    s, _ = fmgen.generate_fm(5, 60, 8, 2, 12)
+    for l, d in [(6, 1), (8, 2), (9, 2)]:
+        a = orc.find(s, l, d)
+        b = orc.find64(s, l, d)
+        assert b.status == 0 and b.codes.tolist() == a.codes.tolist() and b.c_alg == a.c_alg
+    assert orc.find64(s, 32, 1).status == orc.E_ARG  # l <= 31
+    assert orc.find(s, 17, 1).status == orc.E_ARG    # the u32 API keeps l <= 16
+
+
+def test_decode_l31(orc):
+    rng = random.Random(31)
+    for _ in range(200):
+        l = rng.randint(17, 31)
+        x = "".join(rng.choice(ACGT) for _ in range(l))
+        assert orc.decode(rank_of(x), l) == x
+
+
+@pytest.mark.parametrize("l,d", [(20, 1), (24, 2), (31, 1)])
+def test_large_l_hamming_ball_on_ranges(orc, l, d):
+    """n=1, t=l: the result is the Hamming ball of the string.  For every ball
+    member c (enumerated here by mutating the string), the oracle over the
+    range [c-3, c+4) returns exactly the ball members in that range."""
+    rng = random.Random(l * 7 + d)
+    x = "".join(rng.choice(ACGT) for _ in range(l))
+    ball = {x}
+    frontier = {x}
+    for _ in range(d):
+        nxt = set()
+        for y in frontier:
+            for p in range(l):
+                for ch in ACGT:
+                    if ch != y[p]:
+                        nxt.add(y[:p] + ch + y[p + 1:])
+        ball |= nxt
+        frontier = nxt
+    ball_codes = {rank_of(y) for y in ball}
+    assert len(ball_codes) == ball_volume(l, d)
+    s = fmgen.from_strings([x])
+    for c in rng.sample(sorted(ball_codes), 25):
+        lo, hi = max(c - 3, 0), min(c + 4, 4 ** l)
+        got = orc.find64(s, l, d, lo=lo, hi=hi).codes.tolist()
+        assert got == sorted(v for v in ball_codes if lo <= v < hi)
+
+
+def test_large_l_planted_recovery_on_ranges(orc):
+    for seed in range(3):
+        s, rec = fmgen.generate_fm(8, 100, 18, 3, 40 + seed)
+        c = rank_of(rec.consensus)
+        r = orc.find64(s, 18, 3, lo=c - 2000, hi=c + 2000)
+        assert c in set(r.codes.tolist())
+        for m in r.codes.tolist():
+            assert orc.verify_motif(s, 18, 3, m)
