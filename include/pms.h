@@ -14,7 +14,10 @@
  *
  * Codes: A=0 C=1 G=2 T=3; an l-mer's code is big-endian base 4 (first base in
  * the most significant digit), so code order = lexicographic order (SPEC.md:
- * 66-74).  l <= 16, so a code fits uint32.
+ * 66-74).  The uint32-code entry points take l <= 16 (PMS_MAX_L); the
+ * uint64-code ones (pms_find64*, pms_plan_execute64) take l <= 31
+ * (PMS_MAX_L64: "l is capped at 31 so ranks fit a 64-bit
+ * integer").
  *
  * Conventions for every entry point:
  *   - sizes are element counts unless stated; all functions are thread-safe
@@ -42,15 +45,17 @@ extern "C" {
 enum {
     PMS_OK = 0,
     PMS_E_ARG = -1,       /* NULL seqs/count, out_codes NULL with max_out>0,
-                             n<1, t<1, l<1, l>16, l>t, d<0,
-                             lo>hi, plan/shape mismatch */
+                             n<1, t<1, l<1, l>16 (l>31 for the 64-bit
+                             entry points), l>t, d<0, lo>hi,
+                             uint32 output from a plan with l>16 */
     PMS_E_CHAR = -2,      /* a byte outside "ACGTacgt" (incl. 'N') */
     PMS_E_TOO_LARGE = -3, /* n*t or the packed table exceeds 2^31 bytes */
     PMS_E_CUDA = -4,      /* no device, allocation/launch/runtime failure */
     PMS_E_TRUNCATED = -5  /* more motifs than max_out; *count is exact */
 };
 
-#define PMS_MAX_L 16
+#define PMS_MAX_L 16    /* uint32 codes */
+#define PMS_MAX_L64 31  /* uint64 codes */
 
 /* Launch overrides (all 0 = automatic).  Results never depend on them. */
 typedef struct pms_launch {
@@ -75,7 +80,9 @@ typedef struct pms_launch {
     int32_t handoff;         /* block family: a block with at most this many
                                 live candidates finishes them one by one
                                 (0 = auto)                                   */
-    int32_t reserved[1];
+    int32_t wide_words;      /* 1 = 64-bit window words (two 32-bit bit
+                                planes) even for l <= 16; automatic for
+                                l > 16.  Same result                         */
 } pms_launch;
 
 /* Kernel families (pms_launch.algo).  Every family returns the same set.
@@ -139,6 +146,24 @@ int pms_find_ex(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
                 pms_stats *stats);
 
 /* ---------------------------------------------------------------------
+ * pms_find64 / pms_find64_ex -- the same operation with uint64 codes for
+ * l <= 31.  Arguments, ownership, status
+ * order and range semantics are those of pms_find / pms_find_ex, with
+ * out_codes a host array of uint64 (capacity max_out) and hi clipped to
+ * 4^l <= 2^62.  Every l in [1, 31] is accepted (l <= 16 gives the same set as
+ * pms_find, widened).  Windows are packed into 64-bit words (two 32-bit bit
+ * planes); the table is n * ceil32(t-l+1) * 8 bytes.  Exhaustive enumeration
+ * of 4^l candidates is the caller's budget: use [lo, hi) ranges for large l.
+ * ------------------------------------------------------------------- */
+int pms_find64(const uint8_t *seqs, int32_t n, int32_t t, int32_t l, int32_t d,
+               uint64_t *out_codes, uint64_t max_out, uint64_t *count);
+
+int pms_find64_ex(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
+                  int32_t d, uint64_t lo, uint64_t hi, const pms_launch *launch,
+                  uint64_t *out_codes, uint64_t max_out, uint64_t *count,
+                  pms_stats *stats);
+
+/* ---------------------------------------------------------------------
  * Plans: device-resident, asynchronous form for callers that own device
  * memory and streams (the Python binding passes torch tensors and
  * torch.cuda.current_stream()).  A plan holds the packed window table, the
@@ -146,7 +171,9 @@ int pms_find_ex(const uint8_t *seqs, int32_t n, int32_t t, int32_t l,
  * ------------------------------------------------------------------- */
 typedef struct pms_plan pms_plan;
 
-/* Allocates device workspace for the shape.  *plan receives the handle. */
+/* Allocates device workspace for the shape (1 <= l <= 31; plans with l > 16
+ * use 64-bit window words and must be executed with pms_plan_execute64).
+ * *plan receives the handle. */
 int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
                     const pms_launch *launch, pms_plan **plan);
 
@@ -161,6 +188,13 @@ int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
 int pms_plan_execute(pms_plan *plan, const uint8_t *d_seqs, uint64_t lo,
                      uint64_t hi, uint32_t *d_out, uint64_t cap,
                      uint64_t *d_count, void *stream);
+
+/* pms_plan_execute with uint64 result codes (d_out: device, capacity `cap`
+ * uint64 codes); valid for every plan (1 <= l <= 31).  pms_plan_execute on a
+ * plan with l > 16 returns PMS_E_ARG. */
+int pms_plan_execute64(pms_plan *plan, const uint8_t *d_seqs, uint64_t lo,
+                       uint64_t hi, uint64_t *d_out, uint64_t cap,
+                       uint64_t *d_count, void *stream);
 
 /* Waits for the plan's last execution; returns PMS_E_CHAR if the pre-pass
  * saw an invalid byte (the search then did no work and *d_count is 0),

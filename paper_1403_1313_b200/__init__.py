@@ -18,9 +18,10 @@ from ._build import LIB, build
 
 OK, E_ARG, E_CHAR, E_TOO_LARGE, E_CUDA, E_TRUNCATED = 0, -1, -2, -3, -4, -5
 ALGO_AUTO, ALGO_CANDIDATE, ALGO_BLOCK = 0, 1, 2
-MAX_L = 16
+MAX_L = 16     # uint32 codes (pms_find, pms_find_ex, pms_plan_execute)
+MAX_L64 = 31   # uint64 codes (pms_find64, pms_find64_ex, pms_plan_execute64)
 
-__all__ = ["find", "find_ex", "Plan", "Launch", "Stats", "roofline", "device_info", "strerror",
+__all__ = ["find", "find_ex", "find64", "find64_ex", "Plan", "Launch", "Stats", "roofline", "device_info", "strerror",
            "PmsError", "load", "build", "decode_code", "LIB"]
 
 
@@ -38,7 +39,7 @@ class Launch(ctypes.Structure):
                 ("force_generic", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
                 ("no_skip", ctypes.c_int32), ("algo", ctypes.c_int32),
                 ("block_digits", ctypes.c_int32), ("table_global", ctypes.c_int32),
-                ("handoff", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
+                ("handoff", ctypes.c_int32), ("wide_words", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -75,11 +76,18 @@ def load() -> ctypes.CDLL:
         lib.pms_find_ex.argtypes = [u8p, i32, i32, i32, i32, u64, u64, ctypes.POINTER(Launch),
                                     u32p, u64, u64p, ctypes.POINTER(Stats)]
         lib.pms_find_ex.restype = ctypes.c_int
+        lib.pms_find64.argtypes = [u8p, i32, i32, i32, i32, u64p, u64, u64p]
+        lib.pms_find64.restype = ctypes.c_int
+        lib.pms_find64_ex.argtypes = [u8p, i32, i32, i32, i32, u64, u64, ctypes.POINTER(Launch),
+                                      u64p, u64, u64p, ctypes.POINTER(Stats)]
+        lib.pms_find64_ex.restype = ctypes.c_int
         lib.pms_plan_create.argtypes = [i32, i32, i32, i32, ctypes.POINTER(Launch),
                                         ctypes.POINTER(vp)]
         lib.pms_plan_create.restype = ctypes.c_int
         lib.pms_plan_execute.argtypes = [vp, vp, u64, u64, vp, u64, vp, vp]
         lib.pms_plan_execute.restype = ctypes.c_int
+        lib.pms_plan_execute64.argtypes = [vp, vp, u64, u64, vp, u64, vp, vp]
+        lib.pms_plan_execute64.restype = ctypes.c_int
         lib.pms_plan_wait.argtypes = [vp, ctypes.POINTER(Stats)]
         lib.pms_plan_wait.restype = ctypes.c_int
         lib.pms_plan_destroy.argtypes = [vp]
@@ -129,38 +137,62 @@ class FindResult:
     stats: Stats | None = None
 
 
-def find_ex(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
-            launch: Launch | None = None, max_out: int = 1 << 20,
-            want_stats: bool = True) -> FindResult:
-    """One call of pms_find_ex from host buffers; returns the raw status."""
+def _find_ex(fname, ctype, seqs, l, d, lo, hi, launch, max_out, want_stats) -> FindResult:
     lib = load()
     a = _rows(seqs)
     n, t = a.shape
     if hi is None:
         hi = (1 << 64) - 1
-    out = np.empty(max(int(max_out), 1), dtype=np.uint32)
+    out = np.empty(max(int(max_out), 1), dtype=np.uint32 if ctype is ctypes.c_uint32 else np.uint64)
     cnt = ctypes.c_uint64(0)
     st = Stats() if want_stats else None
-    status = lib.pms_find_ex(a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), n, t, l, d,
-                             int(lo), int(hi), ctypes.byref(launch) if launch else None,
-                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), int(max_out),
-                             ctypes.byref(cnt), ctypes.byref(st) if st is not None else None)
+    status = getattr(lib, fname)(a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), n, t, l, d,
+                                 int(lo), int(hi), ctypes.byref(launch) if launch else None,
+                                 out.ctypes.data_as(ctypes.POINTER(ctype)), int(max_out),
+                                 ctypes.byref(cnt), ctypes.byref(st) if st is not None else None)
     k = min(int(cnt.value), int(max_out)) if status in (OK, E_TRUNCATED) else 0
     return FindResult(status, out[:k].copy(), int(cnt.value), st)
+
+
+def find_ex(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
+            launch: Launch | None = None, max_out: int = 1 << 20,
+            want_stats: bool = True) -> FindResult:
+    """One call of pms_find_ex (uint32 codes, l <= 16) from host buffers;
+    returns the raw status."""
+    return _find_ex("pms_find_ex", ctypes.c_uint32, seqs, l, d, lo, hi, launch, max_out,
+                    want_stats)
+
+
+def find64_ex(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
+              launch: Launch | None = None, max_out: int = 1 << 20,
+              want_stats: bool = True) -> FindResult:
+    """One call of pms_find64_ex (uint64 codes, l <= 31) from host buffers."""
+    return _find_ex("pms_find64_ex", ctypes.c_uint64, seqs, l, d, lo, hi, launch, max_out,
+                    want_stats)
+
+
+def _find_all(fx, name, seqs, l, d, lo, hi, launch) -> np.ndarray:
+    cap = 1 << 16
+    while True:
+        r = fx(seqs, l, d, lo, hi, launch, max_out=cap, want_stats=False)
+        if r.status == E_TRUNCATED and r.count > cap:
+            cap = r.count
+            continue
+        if r.status != OK:
+            raise PmsError(r.status, name)
+        return r.codes
 
 
 def find(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
          launch: Launch | None = None) -> np.ndarray:
     """All motif codes (ascending uint32) of seqs for (l, d); raises PmsError."""
-    cap = 1 << 16
-    while True:
-        r = find_ex(seqs, l, d, lo, hi, launch, max_out=cap, want_stats=False)
-        if r.status == E_TRUNCATED and r.count > cap:
-            cap = r.count
-            continue
-        if r.status != OK:
-            raise PmsError(r.status, "pms_find_ex")
-        return r.codes
+    return _find_all(find_ex, "pms_find_ex", seqs, l, d, lo, hi, launch)
+
+
+def find64(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,
+           launch: Launch | None = None) -> np.ndarray:
+    """All motif codes (ascending uint64) for l <= 31 over [lo, hi); raises PmsError."""
+    return _find_all(find64_ex, "pms_find64_ex", seqs, l, d, lo, hi, launch)
 
 
 def decode_code(code: int, l: int) -> str:
@@ -181,18 +213,21 @@ class Plan:
             raise PmsError(s, "pms_plan_create")
 
     def execute(self, d_seqs_ptr: int, lo: int, hi: int, d_out_ptr: int, cap: int,
-                d_count_ptr: int, stream: int = 0) -> None:
-        s = self._lib.pms_plan_execute(self._h, ctypes.c_void_p(d_seqs_ptr), int(lo), int(hi),
-                                       ctypes.c_void_p(d_out_ptr) if d_out_ptr else None,
-                                       int(cap), ctypes.c_void_p(d_count_ptr),
-                                       ctypes.c_void_p(stream) if stream else None)
+                d_count_ptr: int, stream: int = 0, wide: bool = False) -> None:
+        """pms_plan_execute (uint32 codes), or pms_plan_execute64 with wide=True."""
+        fname = "pms_plan_execute64" if wide else "pms_plan_execute"
+        s = getattr(self._lib, fname)(self._h, ctypes.c_void_p(d_seqs_ptr), int(lo), int(hi),
+                                      ctypes.c_void_p(d_out_ptr) if d_out_ptr else None,
+                                      int(cap), ctypes.c_void_p(d_count_ptr),
+                                      ctypes.c_void_p(stream) if stream else None)
         if s != OK:
-            raise PmsError(s, "pms_plan_execute")
+            raise PmsError(s, fname)
 
     def execute_tensors(self, seqs, out, count, lo: int = 0, hi: int | None = None,
                         stream=None) -> None:
         """torch tensors on the current device: seqs uint8 [n,t], out int32/uint32
-        [cap], count int64 [1]; stream defaults to torch's current stream."""
+        [cap] (or int64/uint64 [cap]: 64-bit codes, required for l > 16), count
+        int64 [1]; stream defaults to torch's current stream."""
         import torch
         if stream is None:
             stream = torch.cuda.current_stream()
@@ -200,8 +235,10 @@ class Plan:
         assert tuple(seqs.shape) == (self.n, self.t)
         assert count.dtype == torch.int64 and count.numel() >= 1 and count.is_cuda
         hi = 4 ** self.l if hi is None else hi
+        wide = out.element_size() == 8
+        assert out.is_cuda and out.element_size() in (4, 8)
         self.execute(seqs.data_ptr(), lo, hi, out.data_ptr() if out.numel() else 0, out.numel(),
-                     count.data_ptr(), stream.cuda_stream)
+                     count.data_ptr(), stream.cuda_stream, wide=wide)
 
     def wait(self) -> tuple[int, Stats]:
         st = Stats()

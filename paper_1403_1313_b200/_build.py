@@ -11,11 +11,13 @@ LIB_RELEASE = os.path.join(PKG, "libpms_b200.so")
 LIB_DEBUG = os.path.join(PKG, "libpms_b200_debug.so")  # -DPMS_DEBUG_CHECKS (bounds counters)
 # PMS_DEBUG_LIB=1 selects the bounds-checked build for this process
 LIB = LIB_DEBUG if os.environ.get("PMS_DEBUG_LIB") == "1" else LIB_RELEASE
-SOURCES = [os.path.join(CSRC, "pms.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "pms_device.cuh"), os.path.join(ROOT, "include", "pms.h")]
+# pms.cu: 32-bit-word kernels + host code; pms64.cu: 64-bit-word kernels (l <= 31)
+SOURCES = [os.path.join(CSRC, "pms.cu"), os.path.join(CSRC, "pms64.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, "pms_device.cuh"), os.path.join(CSRC, "pms_kernels.cuh"),
+                  os.path.join(ROOT, "include", "pms.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-O3"]
+              "-Xcompiler", "-fPIC", "-Xptxas", "-O3"]
 
 
 def _nvcc() -> str:
@@ -33,13 +35,31 @@ def stale(lib: str = LIB) -> bool:
 
 
 def _compile(lib: str, extra: list[str], verbose: bool) -> None:
-    tmp = lib + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *SOURCES, "-o", tmp]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
-    os.replace(tmp, lib)
+    """nvcc -c of every translation unit in parallel, then one nvcc -shared link."""
+    tag = f".tmp{os.getpid()}"
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = lib + "." + os.path.splitext(os.path.basename(src))[0] + tag + ".o"
+        cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+               "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        objs.append(obj)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    try:
+        for cmd, pr in procs:
+            if pr.wait() != 0:
+                raise subprocess.CalledProcessError(pr.returncode, cmd)
+        tmp = lib + tag
+        cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+        os.replace(tmp, lib)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
 
 
 def build(force: bool = False, verbose: bool = False, debug: bool | None = None) -> str:

@@ -23,7 +23,7 @@ namespace pms {
 // host reads the counter with pms_debug_violations().  No trap, so a bad index
 // cannot fault the device.  Release builds compile the checks away.
 #ifdef PMS_DEBUG_CHECKS
-__device__ unsigned int g_pms_violations;
+static __device__ unsigned int g_pms_violations;  // one per translation unit
 #define PMS_CHECK(cond)                                          \
     do {                                                         \
         if (!(cond)) atomicAdd(&::pms::g_pms_violations, 1u);    \

@@ -1,0 +1,512 @@
+// pms_kernels.cuh -- the search kernels shared by both window-word widths.
+//
+// Included by pms.cu (32-bit words, l <= 16) and pms64.cu (64-bit words,
+// l <= 31); each translation unit instantiates its own word policy, so the
+// kernel templates live in an anonymous namespace (TU-local stubs) while the
+// argument / table types shared with the host code live in namespace pms.
+//
+// Word policies:
+//   Bp32  one uint32 per window: H plane in bits 16..31, L plane in 0..15;
+//         distances come out doubled (popc over both rotated halves).
+//   Bp64  one uint2 per window: .x = H plane, .y = L plane, position j of the
+//         l-mer at bit l-1-j of each plane (l <= 31); the
+//         distance is popc((cH ^ wH) | (cL ^ wL)) (PAPER.md:63 Hamming).
+// Both expose a candidate as a uint2 register pair so a compare is always
+// popc((c.x ^ e.x) | (c.y ^ e.y)) on an "expanded" window e.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pms_device.cuh"
+
+namespace pms {
+
+struct SearchArgs {
+    const void* tab;                // packed table [n][Wp] of P::word (global)
+    int n, W, Wp;
+    uint32_t dd;                    // threshold in policy units: d << P::kShift (d <= l)
+    unsigned long long lo, hi;      // candidate code range [lo, hi)
+    unsigned long long lo_al;       // lo rounded down to the plan unit (256 or 4^S)
+    unsigned long long span;        // hi - lo_al
+    int batch;                      // candidates per atomic grab (multiple of the unit)
+    int in_smem;                    // stage the table into shared memory (TMA bulk)
+    int skip;                       // 1 = skip rule (skip-BF); 0 = plain brute force
+    int handoff;                    // block family: <= this many survivors -> per-candidate
+    int out_wide;                   // 1 = result codes are uint64, 0 = uint32
+    uint32_t tab_bytes;
+    DevState* st;
+    unsigned long long* nout;       // result counter (caller's d_count)
+    void* out;                      // result buffer, capacity cap (uint32 or uint64)
+    unsigned long long cap;
+};
+
+using SearchFn = void (*)(SearchArgs);
+using PackFn = void (*)(const uint8_t*, int, int, int, int, int, void*, DevState*);
+
+struct BlockKernel {
+    int S, NW;
+    SearchFn fn_smem, fn_global;
+};
+
+constexpr int kBlock = 256;        // threads per CTA of the candidate family (8 warps)
+constexpr int kBlockB = 512;       // max threads per CTA of the block family
+constexpr int kUnitMax = 4096;     // largest block (S = 6)
+constexpr int kBlkMinL = 5;        // the block family needs l >= 5
+constexpr int kReg0Max = 24;       // block family: sequence 0 in registers up to 24 windows/lane
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// 64-bit code (l <= 31) -> 32-bit plane of its even bits
+__host__ __device__ __forceinline__ uint32_t compress_even64(unsigned long long c) {
+    return compress_even((uint32_t)c) | (compress_even((uint32_t)(c >> 32)) << 16);
+}
+
+struct Bp32 {
+    using word = uint32_t;
+    static constexpr int kShift = 1;
+    static constexpr int kMaxL = 16;
+    __device__ static __forceinline__ uint2 prep(unsigned long long code) {
+        const uint32_t c = code_to_bp((uint32_t)code);
+        return make_uint2(c, rot16(c));
+    }
+    __device__ static __forceinline__ uint2 expand(word w) { return make_uint2(w, rot16(w)); }
+    template <int S>
+    __device__ static __forceinline__ uint2 expand_prefix(word w) {
+        constexpr uint32_t M = (1u << S) - 1u;
+        const uint32_t m = w & ~(M | (M << 16));
+        return make_uint2(m, rot16(m));
+    }
+    // doubled Hamming distance of the prefix (positions before the last S)
+    template <int S>
+    __device__ static __forceinline__ uint32_t prefix_dist(uint2 c, word w) {
+        constexpr uint32_t M = (1u << S) - 1u;
+        const uint32_t x = (c.x ^ w) & ~(M | (M << 16));
+        return __popc(x | rot16(x));
+    }
+    template <int S>
+    __device__ static __forceinline__ uint32_t sfx_h(word w) { return (w >> 16) & ((1u << S) - 1u); }
+    template <int S>
+    __device__ static __forceinline__ uint32_t sfx_l(word w) { return w & ((1u << S) - 1u); }
+    // pre-pass: planes of one window -> word
+    __device__ static __forceinline__ word pack(uint32_t H, uint32_t L) { return (H << 16) | L; }
+};
+
+struct Bp64 {
+    using word = uint2;
+    static constexpr int kShift = 0;
+    static constexpr int kMaxL = 31;
+    __device__ static __forceinline__ uint2 prep(unsigned long long code) {
+        return make_uint2(compress_even64(code >> 1), compress_even64(code));
+    }
+    __device__ static __forceinline__ uint2 expand(word w) { return w; }
+    template <int S>
+    __device__ static __forceinline__ uint2 expand_prefix(word w) {
+        constexpr uint32_t M = (1u << S) - 1u;
+        return make_uint2(w.x & ~M, w.y & ~M);
+    }
+    template <int S>
+    __device__ static __forceinline__ uint32_t prefix_dist(uint2 c, word w) {
+        return __popc(((c.x ^ w.x) | (c.y ^ w.y)) >> S);
+    }
+    template <int S>
+    __device__ static __forceinline__ uint32_t sfx_h(word w) { return w.x & ((1u << S) - 1u); }
+    template <int S>
+    __device__ static __forceinline__ uint32_t sfx_l(word w) { return w.y & ((1u << S) - 1u); }
+    __device__ static __forceinline__ word pack(uint32_t H, uint32_t L) { return make_uint2(H, L); }
+};
+
+}  // namespace pms
+
+namespace {
+
+using namespace pms;
+
+// policy-unit distance of a prepared candidate and an expanded window
+__device__ __forceinline__ uint32_t dist(uint2 c, uint2 e) { return __popc((c.x ^ e.x) | (c.y ^ e.y)); }
+
+// ------------------------------------------------------------------ a2 pre-pass
+// One thread per (sequence i, window k < Wp).  Window k (the length-l
+// substring starting at k, k in [0, W)) is packed into a bit-plane word; rows
+// are padded to Wp with copies of window W-1, which cannot change "some window
+// is within d".  Every byte lies in at least one window, so the byte check
+// covers the whole input.
+template <class P>
+__global__ void pms_pack_kernel(const uint8_t* __restrict__ seqs, int n, int t, int l, int W,
+                                int Wp, void* __restrict__ tab_, DevState* st) {
+    typename P::word* tab = static_cast<typename P::word*>(tab_);
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= (long long)n * Wp) return;
+    const int i = (int)(idx / Wp);
+    const int k = (int)(idx - (long long)i * Wp);
+    const uint8_t* p = seqs + (long long)i * t + min(k, W - 1);
+    uint32_t H = 0, L = 0, bad = 0;
+    PMS_CHECK(min(k, W - 1) + l <= t);
+    for (int j = 0; j < l; ++j) {
+        const uint32_t u = p[j] & 0xDFu;  // upper-case; only 'x'/'X' map to 'X'
+        const uint32_t code = u == 'A' ? 0u : u == 'C' ? 1u : u == 'G' ? 2u : u == 'T' ? 3u : 4u;
+        bad |= code >> 2;
+        H = (H << 1) | ((code >> 1) & 1u);
+        L = (L << 1) | (code & 1u);
+    }
+    tab[idx] = P::pack(H, L);
+    if (bad) atomicOr(&st->bad, 1u);
+}
+
+// ------------------------------------------------------------- shared pieces
+// Stage the packed table into shared memory with one TMA bulk copy per 64 KB,
+// completion tracked by an mbarrier (transaction bytes).
+__device__ __forceinline__ void issue_table_copy(const SearchArgs& a, void* stab, uint64_t* bar) {
+    mbar_expect_tx(bar, a.tab_bytes);
+    constexpr uint32_t kChunk = 65536;
+    for (uint32_t off = 0; off < a.tab_bytes; off += kChunk)
+        tma_bulk_g2s(static_cast<char*>(stab) + off, static_cast<const char*>(a.tab) + off,
+                     min(kChunk, a.tab_bytes - off), bar);
+}
+
+__device__ __forceinline__ void stage_table(const SearchArgs& a, void* stab, uint64_t* bar) {
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) issue_table_copy(a, stab, bar);
+    mbar_wait(bar, 0);
+}
+
+// a4+a5 for sequences [i0, n) with the whole warp on one candidate: lanes take
+// windows k = lane, lane+32, ...; one vote per sequence; the first sequence
+// with no window within d abandons the candidate (skip rule).
+template <class P>
+__device__ __forceinline__ bool check_sequences(const typename P::word* tab, int i0, int n, int Wp,
+                                                uint2 cb, uint32_t dd, int lane,
+                                                unsigned long long& scanned, bool skip = true) {
+    bool all = true;
+    for (int i = i0; i < n; ++i) {
+        const typename P::word* row = tab + (size_t)i * Wp;
+        uint32_t m = 0xFFu;
+#pragma unroll 4
+        for (int k = lane; k < Wp; k += 32) {
+            PMS_CHECK(i < n && k < Wp);
+            m = min(m, dist(cb, P::expand(row[k])));
+        }
+        ++scanned;
+        if (!__any_sync(kFull, m <= dd)) {
+            all = false;
+            if (skip) return false;  // skip rule: abandon at the first failing sequence
+        }
+    }
+    return all;
+}
+
+// a6: result store (uint32 or uint64 codes) and atomic-append compaction
+__device__ __forceinline__ void store_code(const SearchArgs& a, unsigned long long slot,
+                                           unsigned long long code) {
+    if (slot >= a.cap) return;
+    if (a.out_wide) static_cast<unsigned long long*>(a.out)[slot] = code;
+    else static_cast<uint32_t*>(a.out)[slot] = (uint32_t)code;
+}
+
+__device__ __forceinline__ void append(const SearchArgs& a, unsigned long long code) {
+    store_code(a, atomicAdd(a.nout, 1ull), code);
+}
+
+// Generic candidate-family variant (any W; table in shared or global memory):
+// the whole warp takes one candidate and scans sequences 0..n-1 with the skip
+// rule (or, with a.skip == 0, without it: the plain brute force the skip rule
+// enhances).
+template <class P, bool SMEM>
+__global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
+    using word = typename P::word;
+    extern __shared__ __align__(128) unsigned char gsm[];
+    __shared__ __align__(8) uint64_t bar;
+    if (*(volatile unsigned int*)&a.st->bad) return;
+    if (SMEM) stage_table(a, gsm, &bar);
+    const word* tab = SMEM ? reinterpret_cast<const word*>(gsm) : static_cast<const word*>(a.tab);
+    const int lane = threadIdx.x & 31;
+    constexpr int kSub = 256;
+    unsigned long long scanned = 0;
+    for (;;) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(&a.st->next, (unsigned long long)a.batch);
+        b = __shfl_sync(kFull, b, 0);
+        if (b >= a.span) break;
+        for (int sb = 0; sb < a.batch; sb += kSub) {
+            const unsigned long long cbase = a.lo_al + b + sb;
+            if (cbase >= a.hi) break;
+            for (int it = 0; it < kSub; ++it) {
+                const unsigned long long code = cbase + it;
+                if (code < a.lo || code >= a.hi) continue;
+                if (check_sequences<P>(tab, 0, a.n, a.Wp, P::prep(code), a.dd, lane, scanned,
+                                       a.skip != 0) &&
+                    lane == 0)
+                    append(a, code);
+            }
+        }
+    }
+    if (lane == 0 && scanned) atomicAdd(&a.st->extra, scanned);
+}
+
+// ------------------------------------------------- PMS_ALGO_BLOCK search
+// The 4^S candidates of a 4^S-aligned code block (S = 5 or 6) share their
+// first l-S digits (the prefix P) and differ in the last S (the suffix x).
+// For a window w, Hamming(P x, w) = Hamming(P, w[0..l-S)) + Hamming(x,
+// w[l-S..l)), so one XOR / OR-fold / POPC of the prefix against w gives p,
+// and the block candidates that match w (distance <= d) are
+// exactly the suffixes within Hamming distance d - p of w's suffix.  After a
+// sequence, alive &= acc (the candidates with a window within d in it); the
+// block is abandoned at the first sequence that leaves no candidate alive --
+// the skip rule on 4^S candidates at once -- and a lone survivor is finished
+// by the whole warp (check_sequences).
+//
+// Candidates are indexed in BIT-PLANE order.  A suffix has planes (H, L) of S
+// bits (H = high bits, L = low bits of its base codes, position l-S in bit
+// S-1); its distance to a window suffix (eH, eL) is popc((H ^ eH) | (L ^ eL)).
+// With X = S - 5: lane = H >> X, mask word k = (H & (2^X-1)) << X | (L >> 5)
+// (4^X words per lane), bit = L & 31.
+//   * a hit with no budget left (p == d, ~80 % of hits) matches only the
+//     window's own suffix: the finding lane sets bit eL & 31 of word
+//     (eH << X) | (eL >> 5) of the warp's shared-memory mask (one atomic OR);
+//   * other hits are broadcast (one SHFL) and every lane ORs, per word, the
+//     table entry T[r-1][eL & 31][mm] with mm = (H ^ eH) | ((L >> 5 ^ eL >> 5) << 5):
+//     bit b set iff popc(mm | (b ^ (eL & 31))) <= r.  mm is the fastest index,
+//     so a broadcast reads (nearly) distinct banks.
+template <int S>
+struct BlkTraits {
+    static constexpr int X = S - 5;
+    static constexpr int C = 1 << (2 * S);               // candidates per block
+    static constexpr int KW = 1 << (2 * X);              // mask words per lane
+    static constexpr uint32_t M = (1u << S) - 1u;        // suffix plane mask
+    static constexpr int TROW = 32 << S;                 // words per budget row
+    static constexpr int TWORDS = S * TROW;              // rows r = 1..S (r = S: all)
+};
+
+template <int S>
+__device__ __forceinline__ void build_suffix_table(uint32_t* T) {
+    using B = BlkTraits<S>;
+    for (int idx = threadIdx.x; idx < B::TWORDS; idx += blockDim.x) {
+        const uint32_t mm = idx & B::M, eL = (idx >> S) & 31;
+        const int r = idx / B::TROW + 1;
+        uint32_t word = 0;
+        for (uint32_t b = 0; b < 32; ++b)
+            if ((int)__popc(mm | (b ^ eL)) <= r) word |= 1u << b;
+        T[idx] = word;
+    }
+}
+
+// Suffix code (S digits, big-endian base 4) of the suffix with planes (H, L).
+__device__ __forceinline__ uint32_t sfx_code(uint32_t h, uint32_t l) {
+    return (spread_even(h) << 1) | spread_even(l);
+}
+
+// Process every pending hit of every lane (hm bits index the lane's windows
+// row[lane + 32*j]) and OR the matching candidates into the lane's acc words.
+template <class P, int S>
+__device__ __forceinline__ void drain_hits(uint32_t hm, const typename P::word* row, int wp,
+                                           uint2 cb, uint32_t dd, int lane, const uint32_t* T,
+                                           uint32_t* wmask,
+                                           uint32_t (&acc)[BlkTraits<S>::KW]) {
+    (void)wp;  // row length (windows), used by the debug bounds checks
+    using B = BlkTraits<S>;
+    while (__any_sync(kFull, hm != 0u)) {
+        uint32_t mine = kFull;
+        if (hm) {
+            const int j = __ffs(hm) - 1;
+            hm &= hm - 1;
+            PMS_CHECK(lane + 32 * j < wp);
+            const typename P::word w = row[lane + 32 * j];
+            const uint32_t p2 = P::template prefix_dist<S>(cb, w);
+            const uint32_t eH = P::template sfx_h<S>(w), eL = P::template sfx_l<S>(w);
+            if (p2 == dd) {
+                PMS_CHECK(((eH << B::X) | (eL >> 5)) < 32u * B::KW);
+                atomicOr(&wmask[(eH << B::X) | (eL >> 5)], 1u << (eL & 31u));
+            } else {  // record: (r-1) row, eL & 31, eH in the low S bits, eL >> 5 on top
+                const uint32_t r = min((dd - p2) >> P::kShift, (uint32_t)S);
+                mine = ((((r - 1) << 5) | (eL & 31u)) << S) | eH | ((eL >> 5) << 24);
+            }
+        }
+        uint32_t who = __ballot_sync(kFull, mine != kFull);
+        while (who) {
+            const int src = __ffs(who) - 1;
+            who &= who - 1;
+            const uint32_t v = __shfl_sync(kFull, mine, src);
+            if (B::X == 0) {
+                PMS_CHECK((v ^ (uint32_t)lane) < (uint32_t)B::TWORDS);
+                acc[0] |= T[v ^ (uint32_t)lane];
+            } else {
+                const uint32_t vx = v & 0x00FFFFFFu, eLt = v >> 24;
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) {
+                    const uint32_t hk = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
+                    const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
+                    PMS_CHECK(((vx ^ hk) | ((lt ^ eLt) << 5)) < (uint32_t)B::TWORDS);
+                    acc[k] |= T[(vx ^ hk) | ((lt ^ eLt) << 5)];
+                }
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < B::KW; ++k) {
+        acc[k] |= wmask[lane * B::KW + k];
+        wmask[lane * B::KW + k] = 0u;
+    }
+    __syncwarp();
+}
+
+// NW > 0: rows are padded to 32*NW windows and the window loops are fully
+// unrolled; for NW <= kReg0Max the lane also keeps windows lane + 32j of
+// sequence 0 in registers, pre-masked (suffix bits cleared) and expanded
+// (larger NW would cost occupancy: all sequences then stream from smem).
+template <class P, int S, bool SMEM, int NW>
+__global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
+    using B = BlkTraits<S>;
+    using word = typename P::word;
+    constexpr bool kReg0 = NW > 0 && NW <= kReg0Max;
+    extern __shared__ __align__(128) uint32_t stab[];  // [T][table if SMEM]
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp single-candidate hits
+    if (*(volatile unsigned int*)&a.st->bad) return;
+    uint32_t* T = stab;
+    uint32_t* wmask = wmasks[threadIdx.x >> 5];
+#pragma unroll
+    for (int k = 0; k < B::KW; ++k) wmask[(threadIdx.x & 31) * B::KW + k] = 0u;
+    word* tsm = reinterpret_cast<word*>(stab + B::TWORDS);  // 128-B aligned for the bulk copy
+    if (SMEM) {  // start the table's TMA bulk copy, build the suffix table meanwhile
+        if (threadIdx.x == 0) mbar_init(&bar, 1);
+        __syncthreads();
+        if (threadIdx.x == 0) issue_table_copy(a, tsm, &bar);
+    }
+    build_suffix_table<S>(T);
+    __syncthreads();
+    if (SMEM) mbar_wait(&bar, 0);
+    const word* tab = SMEM ? tsm : static_cast<const word*>(a.tab);
+    const int lane = threadIdx.x & 31;
+    uint2 wm[kReg0 ? NW : 1];
+#pragma unroll
+    for (int j = 0; j < (kReg0 ? NW : 0); ++j)
+        wm[j] = P::template expand_prefix<S>(tab[min(lane + 32 * j, a.W - 1)]);
+    unsigned long long scanned = 0, bscans = 0;
+
+    for (;;) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(&a.st->next, (unsigned long long)a.batch);
+        b = __shfl_sync(kFull, b, 0);
+        if (b >= a.span) break;
+        for (int sb = 0; sb < a.batch; sb += B::C) {
+            const unsigned long long cbase = a.lo_al + b + sb;
+            if (cbase >= a.hi) break;
+            const uint2 cb = P::prep(cbase);  // suffix bits are zero
+            // this lane's candidates inside [lo, hi)
+            uint32_t alive[B::KW];
+#pragma unroll
+            for (int k = 0; k < B::KW; ++k) alive[k] = kFull;
+            if (cbase < a.lo || cbase + B::C > a.hi) {  // edge block of [lo, hi)
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) {
+                    const uint32_t h = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
+                    const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
+                    uint32_t m = 0u;
+                    for (uint32_t bb = 0; bb < 32; ++bb) {
+                        const unsigned long long c = cbase + sfx_code(h, (lt << 5) | bb);
+                        if (c >= a.lo && c < a.hi) m |= 1u << bb;
+                    }
+                    alive[k] = m;
+                }
+            }
+            int i = 0;
+            bool dead = false;
+            for (; i < a.n; ++i) {
+                if (i > 0 && a.skip) {
+                    int na = 0;
+#pragma unroll
+                    for (int k = 0; k < B::KW; ++k) na += __popc(alive[k]);
+                    if (__reduce_add_sync(kFull, na) <= a.handoff) break;
+                }
+                const word* row = tab + (size_t)i * a.Wp;
+                uint32_t acc[B::KW];
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) acc[k] = 0u;
+                // pass 1: prefix distance of each window; hits recorded per lane
+                if (NW > 0) {
+                    uint32_t hm = 0;
+                    if (kReg0 && i == 0) {
+#pragma unroll
+                        for (int j = 0; j < (kReg0 ? NW : 0); ++j)
+                            if (dist(cb, wm[j]) <= a.dd) hm |= 1u << j;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < NW; ++j) {
+                            PMS_CHECK(lane + 32 * j < a.Wp && i < a.n);
+                            if (P::template prefix_dist<S>(cb, row[lane + 32 * j]) <= a.dd)
+                                hm |= 1u << j;
+                        }
+                    }
+                    // pass 2: resolve the hits into each lane's candidate words
+                    drain_hits<P, S>(hm, row, a.Wp, cb, a.dd, lane, T, wmask, acc);
+                } else {
+                    for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
+                        uint32_t hm = 0;
+                        const int nj = min(a.Wp - k0, 32 * 32) / 32;
+                        for (int j = 0; j < nj; ++j) {
+                            PMS_CHECK(k0 + lane + 32 * j < a.Wp && i < a.n);
+                            if (P::template prefix_dist<S>(cb, row[k0 + lane + 32 * j]) <= a.dd)
+                                hm |= 1u << j;
+                        }
+                        drain_hits<P, S>(hm, row + k0, a.Wp - k0, cb, a.dd, lane, T, wmask, acc);
+                    }
+                }
+                uint32_t any = 0;
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) {
+                    alive[k] &= acc[k];
+                    any |= alive[k];
+                }
+                ++bscans;
+                if (!__any_sync(kFull, any != 0u)) {  // skip rule for the whole block
+                    dead = true;
+                    if (a.skip) break;  // (a.skip == 0: plain brute force scans on)
+                }
+            }
+            if (dead) continue;
+            if (i == a.n) {  // every alive candidate matched all n sequences
+#pragma unroll
+                for (int k = 0; k < B::KW; ++k) {
+                    if (!alive[k]) continue;
+                    const uint32_t h = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
+                    const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
+                    unsigned long long slot = atomicAdd(a.nout, (unsigned long long)__popc(alive[k]));
+                    for (uint32_t m = alive[k]; m; m &= m - 1, ++slot)
+                        store_code(a, slot, cbase + sfx_code(h, (lt << 5) | (__ffs(m) - 1)));
+                }
+                continue;
+            }
+            // at most a.handoff survivors left: the whole warp finishes each one
+            // from sequence i on with the per-candidate check
+            for (;;) {
+                uint32_t pick = kFull;  // (k << 5) | bit of this lane's first alive candidate
+#pragma unroll
+                for (int k = B::KW - 1; k >= 0; --k)
+                    if (alive[k]) pick = ((uint32_t)k << 5) | (__ffs(alive[k]) - 1);
+                const uint32_t holder = __ballot_sync(kFull, pick != kFull);
+                if (!holder) break;
+                const int src = __ffs(holder) - 1;
+                const uint32_t pk = __shfl_sync(kFull, pick, src);
+                const uint32_t k = pk >> 5;
+                if (lane == src) {
+#pragma unroll
+                    for (int q = 0; q < B::KW; ++q)
+                        if (q == (int)k) alive[q] &= alive[q] - 1;  // clear the picked bit
+                }
+                const uint32_t h = ((uint32_t)src << B::X) | (k >> B::X);
+                const uint32_t l5 = ((k & ((1u << B::X) - 1u)) << 5) | (pk & 31u);
+                const unsigned long long code = cbase + sfx_code(h, l5);
+                if (check_sequences<P>(tab, i, a.n, a.Wp, P::prep(code), a.dd, lane, scanned) &&
+                    lane == 0)
+                    append(a, code);
+            }
+        }
+    }
+    if (lane == 0) {
+        if (scanned) atomicAdd(&a.st->extra, scanned);
+        if (bscans) atomicAdd(&a.st->block_scans, bscans);
+    }
+}
+
+}  // namespace

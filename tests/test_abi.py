@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "pms.h")
 def header_functions() -> list[str]:
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(pms_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(pms_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -28,7 +28,8 @@ def lib():
 
 def test_header_declares_the_boundary():
     fns = header_functions()
-    for f in ("pms_find", "pms_find_ex", "pms_plan_create", "pms_plan_execute", "pms_plan_wait",
+    for f in ("pms_find", "pms_find_ex", "pms_find64", "pms_find64_ex", "pms_plan_execute64",
+              "pms_plan_create", "pms_plan_execute", "pms_plan_wait",
               "pms_plan_destroy", "pms_roofline", "pms_strerror", "pms_device_info"):
         assert f in fns
 
@@ -63,6 +64,13 @@ def test_strerror_and_host_argument_checks(lib):
     assert pms.find_ex(s, 9, 1).status == pms.E_ARG      # l > t
     assert pms.find_ex(s, 3, -1).status == pms.E_ARG
     assert pms.find_ex(s, 3, 1, lo=10, hi=5).status == pms.E_ARG
+    # 64-bit codes: l <= 31
+    s40 = np.full((2, 40), ord("A"), np.uint8)
+    assert pms.find64_ex(s40, 32, 1).status == pms.E_ARG
+    assert pms.find64_ex(s40, 0, 1).status == pms.E_ARG
+    assert pms.find64_ex(s, 9, 1).status == pms.E_ARG    # l > t
+    assert pms.find64_ex(s40, 20, -1).status == pms.E_ARG
+    assert pms.find64_ex(s40, 20, 1, lo=10, hi=5).status == pms.E_ARG
 
 
 def _has_gpu() -> bool:
@@ -80,3 +88,7 @@ def test_no_cpu_fallback_without_device(lib):
     assert r.status == pms.E_CUDA
     with pytest.raises(pms.PmsError):
         pms.find(s, 3, 1)
+    s = np.full((2, 40), ord("A"), np.uint8)
+    assert pms.find64_ex(s, 20, 2, lo=0, hi=100).status == pms.E_CUDA
+    with pytest.raises(pms.PmsError):
+        pms.find64(s, 20, 2, lo=0, hi=100)
