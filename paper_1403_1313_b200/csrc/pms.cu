@@ -308,7 +308,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     p->tab_bytes = (uint32_t)((size_t)n * p->Wp * word_bytes);
     const uint32_t static_smem = 12288;  // mbarrier, per-warp hit masks, slack
     const uint32_t ball_bytes =
-        block_algo ? (uint32_t)(S == 6 ? BlkTraits<6>::TWORDS : BlkTraits<5>::TWORDS) * 4u : 0u;
+        block_algo ? (uint32_t)kTWords * 4u : 0u;  // ball table (28 KB)
     p->in_smem = !p->launch.table_global &&
                  p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
     // block family: a table that leaves room for only one CTA per SM is read

@@ -258,34 +258,39 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
 // Candidates are indexed in BIT-PLANE order.  A suffix has planes (H, L) of S
 // bits (H = high bits, L = low bits of its base codes, position l-S in bit
 // S-1); its distance to a window suffix (eH, eL) is popc((H ^ eH) | (L ^ eL)).
-// With X = S - 5: lane = H >> X, mask word k = (H & (2^X-1)) << X | (L >> 5)
-// (4^X words per lane), bit = L & 31.
-//   * a hit with no budget left (p == d, ~80 % of hits) matches only the
-//     window's own suffix: the finding lane sets bit eL & 31 of word
-//     (eH << X) | (eL >> 5) of the warp's shared-memory mask (one atomic OR);
-//   * other hits are broadcast (one SHFL) and every lane ORs, per word, the
-//     table entry T[r-1][eL & 31][mm] with mm = (H ^ eH) | ((L >> 5 ^ eL >> 5) << 5):
-//     bit b set iff popc(mm | (b ^ (eL & 31))) <= r.  mm is the fastest index,
-//     so a broadcast reads (nearly) distinct banks.
+// The last five positions (plane bits 0..4) spread over lanes and bits, the
+// positions above them (S = 6: one) over a lane's mask words:
+//   lane = H & 31, bit = L & 31, word k = (H >> 5) << X | (L >> 5)  (X = S - 5,
+//   4^X words per lane).
+// A hit (window w, prefix distance p <= d, budget r = d - p) matches the
+// block candidates within distance r of w's suffix (eH, eL):
+//   * r = 0 (~80 % of hits) matches only the window's own suffix: the finding
+//     lane sets bit eL & 31 of word k(eH, eL) of lane eH & 31 in the warp's
+//     shared-memory mask (one atomic OR);
+//   * r >= 1: the hit is broadcast (one SHFL) and every lane reads two ball
+//     words of a table T[rho][e][m] (bit b set iff popc(m | (b ^ e)) <= rho,
+//     five positions): A = T[r][eL & 31][lane ^ (eH & 31)] for the word whose
+//     upper position matches w's, B = T[r-1][...] for the other words (one
+//     mismatch spent there).  B is the same for all of a lane's words, so it
+//     goes into one `common` register; A into the one matching word.  m is the
+//     fastest index: a broadcast reads 32 distinct banks.
 template <int S>
 struct BlkTraits {
     static constexpr int X = S - 5;
     static constexpr int C = 1 << (2 * S);               // candidates per block
     static constexpr int KW = 1 << (2 * X);              // mask words per lane
     static constexpr uint32_t M = (1u << S) - 1u;        // suffix plane mask
-    static constexpr int TROW = 32 << S;                 // words per budget row
-    static constexpr int TWORDS = S * TROW;              // rows r = 1..S (r = S: all)
 };
+constexpr int kTRows = 7;                                // rho = 0..6 (5, 6: all ones)
+constexpr int kTWords = kTRows * 1024;                   // 28 KB ball table
 
-template <int S>
 __device__ __forceinline__ void build_suffix_table(uint32_t* T) {
-    using B = BlkTraits<S>;
-    for (int idx = threadIdx.x; idx < B::TWORDS; idx += blockDim.x) {
-        const uint32_t mm = idx & B::M, eL = (idx >> S) & 31;
-        const int r = idx / B::TROW + 1;
+    for (int idx = threadIdx.x; idx < kTWords; idx += blockDim.x) {
+        const uint32_t m = idx & 31u, e = (idx >> 5) & 31u;
+        const int rho = idx >> 10;
         uint32_t word = 0;
         for (uint32_t b = 0; b < 32; ++b)
-            if ((int)__popc(mm | (b ^ eL)) <= r) word |= 1u << b;
+            if ((int)__popc(m | (b ^ e)) <= rho) word |= 1u << b;
         T[idx] = word;
     }
 }
@@ -293,6 +298,13 @@ __device__ __forceinline__ void build_suffix_table(uint32_t* T) {
 // Suffix code (S digits, big-endian base 4) of the suffix with planes (H, L).
 __device__ __forceinline__ uint32_t sfx_code(uint32_t h, uint32_t l) {
     return (spread_even(h) << 1) | spread_even(l);
+}
+
+// Suffix code of the block candidate at (lane, word k, bit b).
+template <int S>
+__device__ __forceinline__ uint32_t blk_sfx(uint32_t lane, uint32_t k, uint32_t b) {
+    constexpr int X = S - 5;
+    return sfx_code(lane | ((k >> X) << 5), b | ((k & ((1u << X) - 1u)) << 5));
 }
 
 // Process every pending hit of every lane (hm bits index the lane's windows
@@ -304,6 +316,9 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const typename P::word* 
                                            uint32_t (&acc)[BlkTraits<S>::KW]) {
     (void)wp;  // row length (windows), used by the debug bounds checks
     using B = BlkTraits<S>;
+    const char* Tb = reinterpret_cast<const char*>(T);
+    const uint32_t lane4 = (uint32_t)lane << 2;
+    uint32_t common = 0u;  // ball words with one upper-position mismatch (all words)
     while (__any_sync(kFull, hm != 0u)) {
         uint32_t mine = kFull;
         if (hm) {
@@ -313,12 +328,13 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const typename P::word* 
             const typename P::word w = row[lane + 32 * j];
             const uint32_t p2 = P::template prefix_dist<S>(cb, w);
             const uint32_t eH = P::template sfx_h<S>(w), eL = P::template sfx_l<S>(w);
+            const uint32_t ek = ((eH >> 5) << B::X) | (eL >> 5);  // word of w's upper position
             if (p2 == dd) {
-                PMS_CHECK(((eH << B::X) | (eL >> 5)) < 32u * B::KW);
-                atomicOr(&wmask[(eH << B::X) | (eL >> 5)], 1u << (eL & 31u));
-            } else {  // record: (r-1) row, eL & 31, eH in the low S bits, eL >> 5 on top
-                const uint32_t r = min((dd - p2) >> P::kShift, (uint32_t)S);
-                mine = ((((r - 1) << 5) | (eL & 31u)) << S) | eH | ((eL >> 5) << 24);
+                PMS_CHECK((((eH & 31u) << (2 * B::X)) | ek) < 32u * B::KW);
+                atomicOr(&wmask[((eH & 31u) << (2 * B::X)) | ek], 1u << (eL & 31u));
+            } else {  // record: byte offset of T[r][eL & 31][eH & 31], word ek on top
+                const uint32_t r = min((dd - p2) >> P::kShift, (uint32_t)(kTRows - 1));
+                mine = ((((r << 10) | ((eL & 31u) << 5) | (eH & 31u)) << 2)) | (ek << 16);
             }
         }
         uint32_t who = __ballot_sync(kFull, mine != kFull);
@@ -326,25 +342,24 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const typename P::word* 
             const int src = __ffs(who) - 1;
             who &= who - 1;
             const uint32_t v = __shfl_sync(kFull, mine, src);
+            const uint32_t off = (v ^ lane4) & 0xFFFFu;
+            PMS_CHECK(off < 4u * kTWords && off >= (B::X ? 4096u : 0u));
+            const uint32_t a = *reinterpret_cast<const uint32_t*>(Tb + off);
             if (B::X == 0) {
-                PMS_CHECK((v ^ (uint32_t)lane) < (uint32_t)B::TWORDS);
-                acc[0] |= T[v ^ (uint32_t)lane];
+                acc[0] |= a;
             } else {
-                const uint32_t vx = v & 0x00FFFFFFu, eLt = v >> 24;
+                common |= *reinterpret_cast<const uint32_t*>(Tb + off - 4096);
+                const uint32_t ek = v >> 16;
 #pragma unroll
-                for (int k = 0; k < B::KW; ++k) {
-                    const uint32_t hk = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
-                    const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
-                    PMS_CHECK(((vx ^ hk) | ((lt ^ eLt) << 5)) < (uint32_t)B::TWORDS);
-                    acc[k] |= T[(vx ^ hk) | ((lt ^ eLt) << 5)];
-                }
+                for (int k = 0; k < B::KW; ++k)
+                    if ((uint32_t)k == ek) acc[k] |= a;
             }
         }
     }
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < B::KW; ++k) {
-        acc[k] |= wmask[lane * B::KW + k];
+        acc[k] |= wmask[lane * B::KW + k] | common;
         wmask[lane * B::KW + k] = 0u;
     }
     __syncwarp();
@@ -359,7 +374,7 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
     using B = BlkTraits<S>;
     using word = typename P::word;
     constexpr bool kReg0 = NW > 0 && NW <= kReg0Max;
-    extern __shared__ __align__(128) uint32_t stab[];  // [T][table if SMEM]
+    extern __shared__ __align__(128) uint32_t stab[];  // [ball table T][window table if SMEM]
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp single-candidate hits
     if (*(volatile unsigned int*)&a.st->bad) return;
@@ -367,13 +382,13 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
     uint32_t* wmask = wmasks[threadIdx.x >> 5];
 #pragma unroll
     for (int k = 0; k < B::KW; ++k) wmask[(threadIdx.x & 31) * B::KW + k] = 0u;
-    word* tsm = reinterpret_cast<word*>(stab + B::TWORDS);  // 128-B aligned for the bulk copy
+    word* tsm = reinterpret_cast<word*>(stab + kTWords);  // 128-B aligned for the bulk copy
     if (SMEM) {  // start the table's TMA bulk copy, build the suffix table meanwhile
         if (threadIdx.x == 0) mbar_init(&bar, 1);
         __syncthreads();
         if (threadIdx.x == 0) issue_table_copy(a, tsm, &bar);
     }
-    build_suffix_table<S>(T);
+    build_suffix_table(T);
     __syncthreads();
     if (SMEM) mbar_wait(&bar, 0);
     const word* tab = SMEM ? tsm : static_cast<const word*>(a.tab);
@@ -400,11 +415,9 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
             if (cbase < a.lo || cbase + B::C > a.hi) {  // edge block of [lo, hi)
 #pragma unroll
                 for (int k = 0; k < B::KW; ++k) {
-                    const uint32_t h = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
-                    const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
                     uint32_t m = 0u;
                     for (uint32_t bb = 0; bb < 32; ++bb) {
-                        const unsigned long long c = cbase + sfx_code(h, (lt << 5) | bb);
+                        const unsigned long long c = cbase + blk_sfx<S>(lane, k, bb);
                         if (c >= a.lo && c < a.hi) m |= 1u << bb;
                     }
                     alive[k] = m;
@@ -469,11 +482,9 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
 #pragma unroll
                 for (int k = 0; k < B::KW; ++k) {
                     if (!alive[k]) continue;
-                    const uint32_t h = ((uint32_t)lane << B::X) | ((uint32_t)k >> B::X);
-                    const uint32_t lt = (uint32_t)k & ((1u << B::X) - 1u);
                     unsigned long long slot = atomicAdd(a.nout, (unsigned long long)__popc(alive[k]));
                     for (uint32_t m = alive[k]; m; m &= m - 1, ++slot)
-                        store_code(a, slot, cbase + sfx_code(h, (lt << 5) | (__ffs(m) - 1)));
+                        store_code(a, slot, cbase + blk_sfx<S>(lane, k, __ffs(m) - 1));
                 }
                 continue;
             }
@@ -494,9 +505,7 @@ __global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
                     for (int q = 0; q < B::KW; ++q)
                         if (q == (int)k) alive[q] &= alive[q] - 1;  // clear the picked bit
                 }
-                const uint32_t h = ((uint32_t)src << B::X) | (k >> B::X);
-                const uint32_t l5 = ((k & ((1u << B::X) - 1u)) << 5) | (pk & 31u);
-                const unsigned long long code = cbase + sfx_code(h, l5);
+                const unsigned long long code = cbase + blk_sfx<S>(src, k, pk & 31u);
                 if (check_sequences<P>(tab, i, a.n, a.Wp, P::prep(code), a.dd, lane, scanned) &&
                     lane == 0)
                     append(a, code);
