@@ -11,6 +11,8 @@ LIB_RELEASE = os.path.join(PKG, "libpms_b200.so")
 LIB_DEBUG = os.path.join(PKG, "libpms_b200_debug.so")  # -DPMS_DEBUG_CHECKS (bounds counters)
 # PMS_DEBUG_LIB=1 selects the bounds-checked build for this process
 LIB = LIB_DEBUG if os.environ.get("PMS_DEBUG_LIB") == "1" else LIB_RELEASE
+# PMS_LIB_OVERRIDE=/path/lib.so loads a variant build (tuning experiments, scripts/variants.py)
+LIB = os.environ.get("PMS_LIB_OVERRIDE") or LIB
 # pms.cu: 32-bit-word kernels + host code; pms64.cu: 64-bit-word kernels (l <= 31)
 SOURCES = [os.path.join(CSRC, "pms.cu"), os.path.join(CSRC, "pms64.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "pms_device.cuh"), os.path.join(CSRC, "pms_kernels.cuh"),

@@ -53,7 +53,17 @@ constexpr int kBlock = 256;        // threads per CTA of the candidate family (8
 constexpr int kBlockB = 512;       // max threads per CTA of the block family
 constexpr int kUnitMax = 4096;     // largest block (S = 6)
 constexpr int kBlkMinL = 5;        // the block family needs l >= 5
-constexpr int kReg0Max = 24;       // block family: sequence 0 in registers up to 24 windows/lane
+// Sequence 0's windows in registers (pre-masked, expanded) for NW <= this:
+// off by default -- the 38 registers it takes at NW = 19 force the drain
+// loop to rematerialise addresses under the 64-register cap (measured at
+// (15,4): 0.563 ms with, 0.520 ms without).
+#ifndef PMS_REG0_MAX
+#define PMS_REG0_MAX 0
+#endif
+#ifndef PMS_BLK_MIN_CTAS
+#define PMS_BLK_MIN_CTAS 2
+#endif
+constexpr int kReg0Max = PMS_REG0_MAX;  // block family: sequence 0 in registers up to this many windows/lane
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 // 64-bit code (l <= 31) -> 32-bit plane of its even bits
@@ -370,7 +380,7 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const typename P::word* 
 // sequence 0 in registers, pre-masked (suffix bits cleared) and expanded
 // (larger NW would cost occupancy: all sequences then stream from smem).
 template <class P, int S, bool SMEM, int NW>
-__global__ void __launch_bounds__(kBlockB, 2) pms_search_block(SearchArgs a) {
+__global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(SearchArgs a) {
     using B = BlkTraits<S>;
     using word = typename P::word;
     constexpr bool kReg0 = NW > 0 && NW <= kReg0Max;
