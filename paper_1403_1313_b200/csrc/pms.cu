@@ -423,6 +423,7 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     SearchArgs a{};
     a.tab = p->d_table; a.n = p->n; a.W = p->W; a.Wp = p->Wp;
     a.dd = (uint32_t)std::min(p->d, p->l) << (p->wide ? Bp64::kShift : Bp32::kShift);
+    a.dp = (uint32_t)std::min(p->d, p->l);
     a.lo = lo; a.hi = hi; a.lo_al = lo_al; a.span = span; a.batch = batch;
     a.in_smem = p->in_smem; a.tab_bytes = p->tab_bytes;
     a.skip = p->launch.no_skip ? 0 : 1;

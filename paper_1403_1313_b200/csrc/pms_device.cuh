@@ -72,6 +72,14 @@ __host__ __device__ __forceinline__ uint32_t bp_to_code(uint32_t w) {
 
 __device__ __forceinline__ uint32_t rot16(uint32_t x) { return __funnelshift_r(x, x, 16); }
 
+// Position of the most significant set bit (x != 0): one FLO, where
+// 31 - __clz(x) costs three instructions.
+__device__ __forceinline__ int msb(uint32_t x) {
+    uint32_t r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return (int)r;
+}
+
 // 2 * Hamming(c, w) for bit-plane words, given the rotated operands.
 __device__ __forceinline__ uint32_t mism2(uint32_t c, uint32_t cr, uint32_t w, uint32_t wr) {
     return __popc((c ^ w) | (cr ^ wr));

@@ -26,6 +26,7 @@ struct SearchArgs {
     const void* tab;                // packed table [n][Wp] of P::word (global)
     int n, W, Wp;
     uint32_t dd;                    // threshold in policy units: d << P::kShift (d <= l)
+    uint32_t dp;                    // block-family prefix threshold: min(d, l) (plain Hamming)
     unsigned long long lo, hi;      // candidate code range [lo, hi)
     unsigned long long lo_al;       // lo rounded down to the plan unit (256 or 4^S)
     unsigned long long span;        // hi - lo_al
@@ -53,17 +54,13 @@ constexpr int kBlock = 256;        // threads per CTA of the candidate family (8
 constexpr int kBlockB = 512;       // max threads per CTA of the block family
 constexpr int kUnitMax = 4096;     // largest block (S = 6)
 constexpr int kBlkMinL = 5;        // the block family needs l >= 5
-// Sequence 0's windows in registers (pre-masked, expanded) for NW <= this:
-// off by default -- the 38 registers it takes at NW = 19 force the drain
-// loop to rematerialise addresses under the 64-register cap (measured at
-// (15,4): 0.563 ms with, 0.520 ms without).
-#ifndef PMS_REG0_MAX
-#define PMS_REG0_MAX 0
-#endif
+// Sequence 0 streams from shared memory like the other sequences: a
+// register-resident copy (38 registers at NW = 19) forced the drain loop to
+// rematerialise addresses under the 64-register cap (measured at (15,4):
+// 0.563 ms with it, 0.520 ms without).
 #ifndef PMS_BLK_MIN_CTAS
 #define PMS_BLK_MIN_CTAS 2
 #endif
-constexpr int kReg0Max = PMS_REG0_MAX;  // block family: sequence 0 in registers up to this many windows/lane
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 // 64-bit code (l <= 31) -> 32-bit plane of its even bits
@@ -80,18 +77,15 @@ struct Bp32 {
         return make_uint2(c, rot16(c));
     }
     __device__ static __forceinline__ uint2 expand(word w) { return make_uint2(w, rot16(w)); }
-    template <int S>
-    __device__ static __forceinline__ uint2 expand_prefix(word w) {
-        constexpr uint32_t M = (1u << S) - 1u;
-        const uint32_t m = w & ~(M | (M << 16));
-        return make_uint2(m, rot16(m));
-    }
-    // doubled Hamming distance of the prefix (positions before the last S)
+    // Hamming distance of the prefix (positions before the last S): with
+    // x = c ^ w, (x | x << 16) holds the per-position mismatch in its upper
+    // half; x << 16 is a multiply (FMA pipe), the OR and the prefix mask are
+    // one LOP3, so the test costs two ALU-pipe ops.
     template <int S>
     __device__ static __forceinline__ uint32_t prefix_dist(uint2 c, word w) {
-        constexpr uint32_t M = (1u << S) - 1u;
-        const uint32_t x = (c.x ^ w) & ~(M | (M << 16));
-        return __popc(x | rot16(x));
+        constexpr uint32_t PM = 0xFFFF0000u & ~(((1u << S) - 1u) << 16);
+        const uint32_t x = c.x ^ w;
+        return __popc((x | (x * 65536u)) & PM);
     }
     template <int S>
     __device__ static __forceinline__ uint32_t sfx_h(word w) { return (w >> 16) & ((1u << S) - 1u); }
@@ -109,11 +103,6 @@ struct Bp64 {
         return make_uint2(compress_even64(code >> 1), compress_even64(code));
     }
     __device__ static __forceinline__ uint2 expand(word w) { return w; }
-    template <int S>
-    __device__ static __forceinline__ uint2 expand_prefix(word w) {
-        constexpr uint32_t M = (1u << S) - 1u;
-        return make_uint2(w.x & ~M, w.y & ~M);
-    }
     template <int S>
     __device__ static __forceinline__ uint32_t prefix_dist(uint2 c, word w) {
         return __popc(((c.x ^ w.x) | (c.y ^ w.y)) >> S);
@@ -317,12 +306,13 @@ __device__ __forceinline__ uint32_t blk_sfx(uint32_t lane, uint32_t k, uint32_t 
     return sfx_code(lane | ((k >> X) << 5), b | ((k & ((1u << X) - 1u)) << 5));
 }
 
-// Process every pending hit of every lane (hm bits index the lane's windows
-// row[lane + 32*j]) and OR the matching candidates into the lane's acc words.
+// Process every pending hit of every lane and OR the matching candidates into
+// the lane's acc words.  Bit q of hm marks window row[lane + 32 * (top - q)]
+// (pass 1 shifts hit flags in from the bottom).
 template <class P, int S>
-__device__ __forceinline__ void drain_hits(uint32_t hm, const typename P::word* row, int wp,
-                                           uint2 cb, uint32_t dd, int lane, const uint32_t* T,
-                                           uint32_t* wmask,
+__device__ __forceinline__ void drain_hits(uint32_t hm, int top, const typename P::word* row,
+                                           int wp, uint2 cb, uint32_t dp, int lane,
+                                           const uint32_t* T, uint32_t* wmask,
                                            uint32_t (&acc)[BlkTraits<S>::KW]) {
     (void)wp;  // row length (windows), used by the debug bounds checks
     using B = BlkTraits<S>;
@@ -332,25 +322,25 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const typename P::word* 
     while (__any_sync(kFull, hm != 0u)) {
         uint32_t mine = kFull;
         if (hm) {
-            const int j = __ffs(hm) - 1;
-            hm &= hm - 1;
-            PMS_CHECK(lane + 32 * j < wp);
-            const typename P::word w = row[lane + 32 * j];
-            const uint32_t p2 = P::template prefix_dist<S>(cb, w);
+            const int q = msb(hm);  // any order
+            hm &= ~(1u << q);
+            PMS_CHECK(lane + 32 * (top - q) < wp && top - q >= 0);
+            const typename P::word w = row[lane + 32 * (top - q)];
+            const uint32_t p = P::template prefix_dist<S>(cb, w);
             const uint32_t eH = P::template sfx_h<S>(w), eL = P::template sfx_l<S>(w);
             const uint32_t ek = ((eH >> 5) << B::X) | (eL >> 5);  // word of w's upper position
-            if (p2 == dd) {
+            if (p == dp) {
                 PMS_CHECK((((eH & 31u) << (2 * B::X)) | ek) < 32u * B::KW);
                 atomicOr(&wmask[((eH & 31u) << (2 * B::X)) | ek], 1u << (eL & 31u));
             } else {  // record: byte offset of T[r][eL & 31][eH & 31], word ek on top
-                const uint32_t r = min((dd - p2) >> P::kShift, (uint32_t)(kTRows - 1));
+                const uint32_t r = min(dp - p, (uint32_t)(kTRows - 1));
                 mine = ((((r << 10) | ((eL & 31u) << 5) | (eH & 31u)) << 2)) | (ek << 16);
             }
         }
         uint32_t who = __ballot_sync(kFull, mine != kFull);
         while (who) {
-            const int src = __ffs(who) - 1;
-            who &= who - 1;
+            const int src = msb(who);
+            who &= ~(1u << src);
             const uint32_t v = __shfl_sync(kFull, mine, src);
             const uint32_t off = (v ^ lane4) & 0xFFFFu;
             PMS_CHECK(off < 4u * kTWords && off >= (B::X ? 4096u : 0u));
@@ -359,10 +349,10 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const typename P::word* 
                 acc[0] |= a;
             } else {
                 common |= *reinterpret_cast<const uint32_t*>(Tb + off - 4096);
-                const uint32_t ek = v >> 16;
+                const uint32_t ekv = v >> 16;
 #pragma unroll
                 for (int k = 0; k < B::KW; ++k)
-                    if ((uint32_t)k == ek) acc[k] |= a;
+                    if ((uint32_t)k == ekv) acc[k] |= a;
             }
         }
     }
@@ -376,14 +366,11 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, const typename P::word* 
 }
 
 // NW > 0: rows are padded to 32*NW windows and the window loops are fully
-// unrolled; for NW <= kReg0Max the lane also keeps windows lane + 32j of
-// sequence 0 in registers, pre-masked (suffix bits cleared) and expanded
-// (larger NW would cost occupancy: all sequences then stream from smem).
+// unrolled; NW = 0: any row length, 32 windows per lane per chunk.
 template <class P, int S, bool SMEM, int NW>
 __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(SearchArgs a) {
     using B = BlkTraits<S>;
     using word = typename P::word;
-    constexpr bool kReg0 = NW > 0 && NW <= kReg0Max;
     extern __shared__ __align__(128) uint32_t stab[];  // [ball table T][window table if SMEM]
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp single-candidate hits
@@ -403,11 +390,8 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
     if (SMEM) mbar_wait(&bar, 0);
     const word* tab = SMEM ? tsm : static_cast<const word*>(a.tab);
     const int lane = threadIdx.x & 31;
-    uint2 wm[kReg0 ? NW : 1];
-#pragma unroll
-    for (int j = 0; j < (kReg0 ? NW : 0); ++j)
-        wm[j] = P::template expand_prefix<S>(tab[min(lane + 32 * j, a.W - 1)]);
     unsigned long long scanned = 0, bscans = 0;
+    const uint32_t dp1 = a.dp + 1u;
 
     for (;;) {
         unsigned long long b = 0;
@@ -446,33 +430,30 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                 uint32_t acc[B::KW];
 #pragma unroll
                 for (int k = 0; k < B::KW; ++k) acc[k] = 0u;
-                // pass 1: prefix distance of each window; hits recorded per lane
+                // pass 1: prefix distance of each window; a hit (p <= d) makes
+                // p - (d + 1) negative, and its sign bit is shifted into hm
+                // (one funnel shift per window, no compare / select)
                 if (NW > 0) {
                     uint32_t hm = 0;
-                    if (kReg0 && i == 0) {
 #pragma unroll
-                        for (int j = 0; j < (kReg0 ? NW : 0); ++j)
-                            if (dist(cb, wm[j]) <= a.dd) hm |= 1u << j;
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < NW; ++j) {
-                            PMS_CHECK(lane + 32 * j < a.Wp && i < a.n);
-                            if (P::template prefix_dist<S>(cb, row[lane + 32 * j]) <= a.dd)
-                                hm |= 1u << j;
-                        }
+                    for (int j = 0; j < NW; ++j) {
+                        PMS_CHECK(lane + 32 * j < a.Wp && i < a.n);
+                        hm = __funnelshift_l(P::template prefix_dist<S>(cb, row[lane + 32 * j]) - dp1,
+                                             hm, 1);
                     }
                     // pass 2: resolve the hits into each lane's candidate words
-                    drain_hits<P, S>(hm, row, a.Wp, cb, a.dd, lane, T, wmask, acc);
+                    drain_hits<P, S>(hm, NW - 1, row, a.Wp, cb, a.dp, lane, T, wmask, acc);
                 } else {
                     for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
                         uint32_t hm = 0;
                         const int nj = min(a.Wp - k0, 32 * 32) / 32;
                         for (int j = 0; j < nj; ++j) {
                             PMS_CHECK(k0 + lane + 32 * j < a.Wp && i < a.n);
-                            if (P::template prefix_dist<S>(cb, row[k0 + lane + 32 * j]) <= a.dd)
-                                hm |= 1u << j;
+                            hm = __funnelshift_l(
+                                P::template prefix_dist<S>(cb, row[k0 + lane + 32 * j]) - dp1, hm, 1);
                         }
-                        drain_hits<P, S>(hm, row + k0, a.Wp - k0, cb, a.dd, lane, T, wmask, acc);
+                        drain_hits<P, S>(hm, nj - 1, row + k0, a.Wp - k0, cb, a.dp, lane, T, wmask,
+                                         acc);
                     }
                 }
                 uint32_t any = 0;
