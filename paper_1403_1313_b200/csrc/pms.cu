@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kBlock) pms_search_reg(SearchArgs a) {
                         const uint32_t hb = (G == 32) ? bal : ((bal >> (16 * h)) & 0xFFFFu);
                         if (hb) {
                             const uint32_t cbh = ubp | c_bp256[it] | (uint32_t)h;
-                            if (check_sequences<Bp32>(tab, 1, a.n, a.Wp, make_uint2(cbh, rot16(cbh)), a.dd,
+                            if (check_sequences<Bp32>(tab, 1, a.n, a.Wp, make_uint2(cbh, rot16(cbh)), a.dp,
                                                           lane, scanned) &&
                                 lane == 0)
                                 append(a, cbase + it + h);
@@ -422,7 +422,7 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
 
     SearchArgs a{};
     a.tab = p->d_table; a.n = p->n; a.W = p->W; a.Wp = p->Wp;
-    a.dd = (uint32_t)std::min(p->d, p->l) << (p->wide ? Bp64::kShift : Bp32::kShift);
+    a.dd = 2u * (uint32_t)std::min(p->d, p->l);
     a.dp = (uint32_t)std::min(p->d, p->l);
     a.lo = lo; a.hi = hi; a.lo_al = lo_al; a.span = span; a.batch = batch;
     a.in_smem = p->in_smem; a.tab_bytes = p->tab_bytes;

@@ -25,8 +25,8 @@ namespace pms {
 struct SearchArgs {
     const void* tab;                // packed table [n][Wp] of P::word (global)
     int n, W, Wp;
-    uint32_t dd;                    // threshold in policy units: d << P::kShift (d <= l)
-    uint32_t dp;                    // block-family prefix threshold: min(d, l) (plain Hamming)
+    uint32_t dd;                    // candidate-family register kernel: 2*min(d, l) (mism2 is doubled)
+    uint32_t dp;                    // every other test: min(d, l) (plain Hamming)
     unsigned long long lo, hi;      // candidate code range [lo, hi)
     unsigned long long lo_al;       // lo rounded down to the plan unit (256 or 4^S)
     unsigned long long span;        // hi - lo_al
@@ -70,13 +70,18 @@ __host__ __device__ __forceinline__ uint32_t compress_even64(unsigned long long 
 
 struct Bp32 {
     using word = uint32_t;
-    static constexpr int kShift = 1;
     static constexpr int kMaxL = 16;
     __device__ static __forceinline__ uint2 prep(unsigned long long code) {
         const uint32_t c = code_to_bp((uint32_t)code);
         return make_uint2(c, rot16(c));
     }
-    __device__ static __forceinline__ uint2 expand(word w) { return make_uint2(w, rot16(w)); }
+    // Hamming distance of a candidate and a window: with x = c ^ w the
+    // upper half of x | x << 16 is the per-position mismatch mask (the
+    // shift is a multiply on the FMA pipe; OR + mask are one LOP3)
+    __device__ static __forceinline__ uint32_t full_dist(uint2 c, word w) {
+        const uint32_t x = c.x ^ w;
+        return __popc((x | (x * 65536u)) & 0xFFFF0000u);
+    }
     // Hamming distance of the prefix (positions before the last S): with
     // x = c ^ w, (x | x << 16) holds the per-position mismatch in its upper
     // half; x << 16 is a multiply (FMA pipe), the OR and the prefix mask are
@@ -97,12 +102,13 @@ struct Bp32 {
 
 struct Bp64 {
     using word = uint2;
-    static constexpr int kShift = 0;
     static constexpr int kMaxL = 31;
     __device__ static __forceinline__ uint2 prep(unsigned long long code) {
         return make_uint2(compress_even64(code >> 1), compress_even64(code));
     }
-    __device__ static __forceinline__ uint2 expand(word w) { return w; }
+    __device__ static __forceinline__ uint32_t full_dist(uint2 c, word w) {
+        return __popc((c.x ^ w.x) | (c.y ^ w.y));
+    }
     template <int S>
     __device__ static __forceinline__ uint32_t prefix_dist(uint2 c, word w) {
         return __popc(((c.x ^ w.x) | (c.y ^ w.y)) >> S);
@@ -120,8 +126,6 @@ namespace {
 
 using namespace pms;
 
-// policy-unit distance of a prepared candidate and an expanded window
-__device__ __forceinline__ uint32_t dist(uint2 c, uint2 e) { return __popc((c.x ^ e.x) | (c.y ^ e.y)); }
 
 // ------------------------------------------------------------------ a2 pre-pass
 // One thread per (sequence i, window k < Wp).  Window k (the length-l
@@ -174,7 +178,7 @@ __device__ __forceinline__ void stage_table(const SearchArgs& a, void* stab, uin
 // with no window within d abandons the candidate (skip rule).
 template <class P>
 __device__ __forceinline__ bool check_sequences(const typename P::word* tab, int i0, int n, int Wp,
-                                                uint2 cb, uint32_t dd, int lane,
+                                                uint2 cb, uint32_t d, int lane,
                                                 unsigned long long& scanned, bool skip = true) {
     bool all = true;
     for (int i = i0; i < n; ++i) {
@@ -183,10 +187,10 @@ __device__ __forceinline__ bool check_sequences(const typename P::word* tab, int
 #pragma unroll 4
         for (int k = lane; k < Wp; k += 32) {
             PMS_CHECK(i < n && k < Wp);
-            m = min(m, dist(cb, P::expand(row[k])));
+            m = min(m, P::full_dist(cb, row[k]));
         }
         ++scanned;
-        if (!__any_sync(kFull, m <= dd)) {
+        if (!__any_sync(kFull, m <= d)) {
             all = false;
             if (skip) return false;  // skip rule: abandon at the first failing sequence
         }
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
             for (int it = 0; it < kSub; ++it) {
                 const unsigned long long code = cbase + it;
                 if (code < a.lo || code >= a.hi) continue;
-                if (check_sequences<P>(tab, 0, a.n, a.Wp, P::prep(code), a.dd, lane, scanned,
+                if (check_sequences<P>(tab, 0, a.n, a.Wp, P::prep(code), a.dp, lane, scanned,
                                        a.skip != 0) &&
                     lane == 0)
                     append(a, code);
@@ -497,7 +501,7 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                         if (q == (int)k) alive[q] &= alive[q] - 1;  // clear the picked bit
                 }
                 const unsigned long long code = cbase + blk_sfx<S>(src, k, pk & 31u);
-                if (check_sequences<P>(tab, i, a.n, a.Wp, P::prep(code), a.dd, lane, scanned) &&
+                if (check_sequences<P>(tab, i, a.n, a.Wp, P::prep(code), a.dp, lane, scanned) &&
                     lane == 0)
                     append(a, code);
             }
