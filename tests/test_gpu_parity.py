@@ -447,3 +447,41 @@ def test_block_algo_handoff_thresholds(orc):
         for h in (1, 2, 5, 40, 5000):
             L = pms.Launch(algo=pms.ALGO_BLOCK, block_digits=S, handoff=h)
             assert gpu(s, 9, 2, launch=L).codes.tolist() == want, (S, h)
+
+
+# --------------------------------- compaction stress (SURVEY 8(d) extra configs)
+
+def test_compaction_stress_10_4(orc):
+    """(10,4), n=20, t=600: nearly every candidate is a motif (~1e6 of 4^10):
+    the atomic-append compaction writes ~1e6 codes; both families; exact
+    count on truncation (max_out = 0 size query, then a too-small buffer)."""
+    s, _ = fmgen.generate_fm(20, 600, 10, 4, 1)
+    want = orc.find(s, 10, 4)
+    assert want.status == 0 and want.count > 900_000
+    for L in (None, CAND, pms.Launch(algo=pms.ALGO_BLOCK, block_digits=6)):
+        got = gpu(s, 10, 4, launch=L, max_out=1 << 21)
+        assert got.status == 0 and got.count == want.count
+        assert np.array_equal(got.codes, want.codes)
+    r = gpu(s, 10, 4, max_out=0)
+    assert r.status == pms.E_TRUNCATED and r.count == want.count
+    r = gpu(s, 10, 4, max_out=want.count - 1)
+    assert r.status == pms.E_TRUNCATED and r.count == want.count
+
+
+def test_compaction_stress_16_6(orc):
+    """(16,6), n=20, t=600: ~1e5 spurious motifs over the full 4^16 space.
+    Exhaustive GPU run; oracle parity on ranges; every sampled motif
+    re-verifies; the planted consensus is present."""
+    s, rec = fmgen.generate_fm(20, 600, 16, 6, 1)
+    full = gpu(s, 16, 6, max_out=1 << 24)
+    assert full.status == 0 and full.count > 10_000
+    got = full.codes.tolist()
+    cons = int("".join(str("ACGT".index(c)) for c in rec.consensus), 4)
+    assert cons in set(got)
+    rng = random.Random(166)
+    for m in rng.sample(got, 50):
+        assert orc.verify_motif(s, 16, 6, m)
+    for lo in [cons - 20000] + [rng.randrange(0, 4 ** 16 - 60000) for _ in range(3)]:
+        hi = lo + 40000
+        want = orc.find(s, 16, 6, lo=lo, hi=hi).codes.tolist()
+        assert [c for c in got if lo <= c < hi] == want
