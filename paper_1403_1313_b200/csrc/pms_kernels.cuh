@@ -96,28 +96,45 @@ struct Bp32 {
     __device__ static __forceinline__ uint32_t sfx_h(word w) { return (w >> 16) & ((1u << S) - 1u); }
     template <int S>
     __device__ static __forceinline__ uint32_t sfx_l(word w) { return w & ((1u << S) - 1u); }
-    // pre-pass: planes of one window -> word
-    __device__ static __forceinline__ word pack(uint32_t H, uint32_t L) { return (H << 16) | L; }
+    // suffix planes (bit S-1 = first suffix base) -> suffix code (S digits)
+    template <int S>
+    __device__ static __forceinline__ uint32_t sfx_code(uint32_t h, uint32_t l) {
+        return (spread_even(h) << 1) | spread_even(l);
+    }
+    // pre-pass: planes of one window (position j at bit l-1-j) -> word
+    __device__ static __forceinline__ word pack(uint32_t H, uint32_t L, int) { return (H << 16) | L; }
 };
 
 struct Bp64 {
     using word = uint2;
     static constexpr int kMaxL = 31;
+    // Planes are TOP-aligned: position j of the l-mer sits at bit 32 - l + j
+    // (the last base in bit 31), so the suffix is the top S bits of each plane
+    // and a left shift -- a multiply, on the FMA pipe -- drops it.
     __device__ static __forceinline__ uint2 prep(unsigned long long code) {
-        return make_uint2(compress_even64(code >> 1), compress_even64(code));
+        return make_uint2(__brev(compress_even64(code >> 1)), __brev(compress_even64(code)));
     }
     __device__ static __forceinline__ uint32_t full_dist(uint2 c, word w) {
         return __popc((c.x ^ w.x) | (c.y ^ w.y));
     }
     template <int S>
     __device__ static __forceinline__ uint32_t prefix_dist(uint2 c, word w) {
-        return __popc(((c.x ^ w.x) | (c.y ^ w.y)) >> S);
+        return __popc(((c.x ^ w.x) | (c.y ^ w.y)) * (1u << S));
     }
+    // suffix planes: bit i = suffix position i (first suffix base in bit 0)
     template <int S>
-    __device__ static __forceinline__ uint32_t sfx_h(word w) { return w.x & ((1u << S) - 1u); }
+    __device__ static __forceinline__ uint32_t sfx_h(word w) { return w.x >> (32 - S); }
     template <int S>
-    __device__ static __forceinline__ uint32_t sfx_l(word w) { return w.y & ((1u << S) - 1u); }
-    __device__ static __forceinline__ word pack(uint32_t H, uint32_t L) { return make_uint2(H, L); }
+    __device__ static __forceinline__ uint32_t sfx_l(word w) { return w.y >> (32 - S); }
+    template <int S>
+    __device__ static __forceinline__ uint32_t sfx_code(uint32_t h, uint32_t l) {
+        return (spread_even(__brev(h) >> (32 - S)) << 1) | spread_even(__brev(l) >> (32 - S));
+    }
+    // pre-pass: planes with position j at bit l-1-j -> position j at bit
+    // 32-l+j (bit reversal)
+    __device__ static __forceinline__ word pack(uint32_t H, uint32_t L, int) {
+        return make_uint2(__brev(H), __brev(L));
+    }
 };
 
 }  // namespace pms
@@ -151,7 +168,7 @@ __global__ void pms_pack_kernel(const uint8_t* __restrict__ seqs, int n, int t, 
         H = (H << 1) | ((code >> 1) & 1u);
         L = (L << 1) | (code & 1u);
     }
-    tab[idx] = P::pack(H, L);
+    tab[idx] = P::pack(H, L, l);
     if (bad) atomicOr(&st->bad, 1u);
 }
 
@@ -298,16 +315,12 @@ __device__ __forceinline__ void build_suffix_table(uint32_t* T) {
     }
 }
 
-// Suffix code (S digits, big-endian base 4) of the suffix with planes (H, L).
-__device__ __forceinline__ uint32_t sfx_code(uint32_t h, uint32_t l) {
-    return (spread_even(h) << 1) | spread_even(l);
-}
-
-// Suffix code of the block candidate at (lane, word k, bit b).
-template <int S>
+// Suffix code (S digits, big-endian base 4) of the block candidate at
+// (lane, word k, bit b).
+template <class P, int S>
 __device__ __forceinline__ uint32_t blk_sfx(uint32_t lane, uint32_t k, uint32_t b) {
     constexpr int X = S - 5;
-    return sfx_code(lane | ((k >> X) << 5), b | ((k & ((1u << X) - 1u)) << 5));
+    return P::template sfx_code<S>(lane | ((k >> X) << 5), b | ((k & ((1u << X) - 1u)) << 5));
 }
 
 // Process every pending hit of every lane and OR the matching candidates into
@@ -415,7 +428,7 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                 for (int k = 0; k < B::KW; ++k) {
                     uint32_t m = 0u;
                     for (uint32_t bb = 0; bb < 32; ++bb) {
-                        const unsigned long long c = cbase + blk_sfx<S>(lane, k, bb);
+                        const unsigned long long c = cbase + blk_sfx<P, S>(lane, k, bb);
                         if (c >= a.lo && c < a.hi) m |= 1u << bb;
                     }
                     alive[k] = m;
@@ -479,7 +492,7 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                     if (!alive[k]) continue;
                     unsigned long long slot = atomicAdd(a.nout, (unsigned long long)__popc(alive[k]));
                     for (uint32_t m = alive[k]; m; m &= m - 1, ++slot)
-                        store_code(a, slot, cbase + blk_sfx<S>(lane, k, __ffs(m) - 1));
+                        store_code(a, slot, cbase + blk_sfx<P, S>(lane, k, __ffs(m) - 1));
                 }
                 continue;
             }
@@ -500,7 +513,7 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                     for (int q = 0; q < B::KW; ++q)
                         if (q == (int)k) alive[q] &= alive[q] - 1;  // clear the picked bit
                 }
-                const unsigned long long code = cbase + blk_sfx<S>(src, k, pk & 31u);
+                const unsigned long long code = cbase + blk_sfx<P, S>(src, k, pk & 31u);
                 if (check_sequences<P>(tab, i, a.n, a.Wp, P::prep(code), a.dp, lane, scanned) &&
                     lane == 0)
                     append(a, code);
