@@ -374,10 +374,20 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, int top, const typename 
         }
     }
     __syncwarp();
+    if (B::KW == 4) {  // the lane's four words in one 16-B access each way
+        uint4* wv = reinterpret_cast<uint4*>(wmask + lane * 4);
+        const uint4 m = *wv;
+        *wv = make_uint4(0u, 0u, 0u, 0u);
+        acc[0] |= m.x | common;
+        acc[B::KW > 1 ? 1 : 0] |= m.y | common;
+        acc[B::KW > 2 ? 2 : 0] |= m.z | common;
+        acc[B::KW > 3 ? 3 : 0] |= m.w | common;
+    } else {
 #pragma unroll
-    for (int k = 0; k < B::KW; ++k) {
-        acc[k] |= wmask[lane * B::KW + k] | common;
-        wmask[lane * B::KW + k] = 0u;
+        for (int k = 0; k < B::KW; ++k) {
+            acc[k] |= wmask[lane * B::KW + k] | common;
+            wmask[lane * B::KW + k] = 0u;
+        }
     }
     __syncwarp();
 }
@@ -390,7 +400,7 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
     using word = typename P::word;
     extern __shared__ __align__(128) uint32_t stab[];  // [ball table T][window table if SMEM]
     __shared__ __align__(8) uint64_t bar;
-    __shared__ uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp single-candidate hits
+    __shared__ __align__(16) uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp r = 0 hits
     if (*(volatile unsigned int*)&a.st->bad) return;
     uint32_t* T = stab;
     uint32_t* wmask = wmasks[threadIdx.x >> 5];
