@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
 //     five positions): A = T[r][eL & 31][lane ^ (eH & 31)] for the word whose
 //     upper position matches w's, B = T[r-1][...] for the other words (one
 //     mismatch spent there).  B is the same for all of a lane's words, so it
-//     goes into one `common` register; A into the one matching word.  m is the
+//     goes into one `common` register; A into the one matching word (an
+//     atomic OR on the lane's own word of the shared mask).  m is the
 //     fastest index: a broadcast reads 32 distinct banks.
 template <int S>
 struct BlkTraits {
@@ -366,10 +367,9 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, int top, const typename 
                 acc[0] |= a;
             } else {
                 common |= *reinterpret_cast<const uint32_t*>(Tb + off - 4096);
-                const uint32_t ekv = v >> 16;
-#pragma unroll
-                for (int k = 0; k < B::KW; ++k)
-                    if ((uint32_t)k == ekv) acc[k] |= a;
+                // A into the lane's own word ek of the shared mask: one
+                // conflict-free atomic instead of a branch tree over acc[k]
+                atomicOr(&wmask[lane * B::KW + (v >> 16)], a);
             }
         }
     }
