@@ -309,14 +309,19 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     const uint32_t static_smem = 12288;  // mbarrier, per-warp hit masks, slack
     const uint32_t ball_bytes =
         block_algo ? (uint32_t)kTWords * 4u : 0u;  // ball table (28 KB)
+    // block family with a register tile: per-warp hit queue (u16 window
+    // indices, 32*NW per warp, sized for the largest CTA)
+    const uint32_t queue_bytes =
+        (block_algo && PMS_QUEUE_DRAIN && bk->NW > 0) ? (uint32_t)(kBlockB / 32) * 64u * bk->NW : 0u;
     p->in_smem = !p->launch.table_global &&
-                 p->tab_bytes + ball_bytes + static_smem <= (uint32_t)smem_optin;
+                 p->tab_bytes + ball_bytes + queue_bytes + static_smem <= (uint32_t)smem_optin;
     // block family: a table that leaves room for only one CTA per SM is read
     // through L1/L2 instead -- two resident CTAs win (measured at (16,5):
     // 8.6 ms vs 9.9 ms); 228 KB of shared memory per SM, 1 KB reserved per CTA
-    if (block_algo && p->in_smem && 2u * (p->tab_bytes + ball_bytes + static_smem + 1024u) > 233472u)
+    if (block_algo && p->in_smem &&
+        2u * (p->tab_bytes + ball_bytes + queue_bytes + static_smem + 1024u) > 233472u)
         p->in_smem = 0;
-    p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0);
+    p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0) + queue_bytes;
 
     RegKernel rk{};
     const int force_g = (p->launch.lanes_per_cand == 16 || p->launch.lanes_per_cand == 32)
@@ -427,7 +432,7 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     a.lo = lo; a.hi = hi; a.lo_al = lo_al; a.span = span; a.batch = batch;
     a.in_smem = p->in_smem; a.tab_bytes = p->tab_bytes;
     a.skip = p->launch.no_skip ? 0 : 1;
-    a.handoff = p->launch.handoff > 0 ? p->launch.handoff : (p->d >= 5 ? 3 : 1);  // measured
+    a.handoff = p->launch.handoff > 0 ? p->launch.handoff : (p->d >= 5 ? 2 : 1);  // measured
     a.st = p->d_state; a.nout = reinterpret_cast<unsigned long long*>(d_count);
     a.out = d_out; a.out_wide = out_wide; a.cap = cap;
 

@@ -392,6 +392,88 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, int top, const typename 
     __syncwarp();
 }
 
+#ifndef PMS_QUEUE_DRAIN
+#define PMS_QUEUE_DRAIN 1
+#endif
+// Balanced drain (NW > 0): the warp's hits are first compacted into a
+// per-warp shared-memory queue of window indices (exclusive prefix sum of the
+// lanes' hit counts, then each lane writes its own), and the queue is
+// processed 32 hits per round -- typically ONE round, where the per-lane
+// drain needs max-over-lanes(hits) rounds of the same work.
+template <class P, int S>
+__device__ __forceinline__ void drain_queue(uint32_t hm, int top, const typename P::word* row,
+                                            uint16_t* queue, uint2 cb, uint32_t dp, int lane,
+                                            const uint32_t* T, uint32_t* wmask,
+                                            uint32_t (&acc)[BlkTraits<S>::KW]) {
+    using B = BlkTraits<S>;
+    const char* Tb = reinterpret_cast<const char*>(T);
+    const uint32_t lane4 = (uint32_t)lane << 2;
+    const uint32_t nh = __popc(hm);
+    uint32_t inc = nh;  // inclusive prefix sum of the hit counts over lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += v;
+    }
+    const uint32_t total = __shfl_sync(kFull, inc, 31);
+    uint32_t pos = inc - nh;
+    while (hm) {
+        const int q = msb(hm);
+        hm &= ~(1u << q);
+        queue[pos++] = (uint16_t)(lane + 32 * (top - q));
+    }
+    __syncwarp();
+    uint32_t common = 0u;  // ball words with one upper-position mismatch (all words)
+    for (uint32_t base = 0; base < total; base += 32) {
+        uint32_t mine = kFull;
+        if (base + lane < total) {
+            const typename P::word w = row[queue[base + lane]];
+            const uint32_t p = P::template prefix_dist<S>(cb, w);
+            const uint32_t eH = P::template sfx_h<S>(w), eL = P::template sfx_l<S>(w);
+            const uint32_t ek = ((eH >> 5) << B::X) | (eL >> 5);  // word of w's upper position
+            if (p == dp) {
+                PMS_CHECK((((eH & 31u) << (2 * B::X)) | ek) < 32u * B::KW);
+                atomicOr(&wmask[((eH & 31u) << (2 * B::X)) | ek], 1u << (eL & 31u));
+            } else {  // record: byte offset of T[r][eL & 31][eH & 31], word ek on top
+                const uint32_t r = min(dp - p, (uint32_t)(kTRows - 1));
+                mine = ((((r << 10) | ((eL & 31u) << 5) | (eH & 31u)) << 2)) | (ek << 16);
+            }
+        }
+        uint32_t who = __ballot_sync(kFull, mine != kFull);
+        while (who) {
+            const int src = msb(who);
+            who &= ~(1u << src);
+            const uint32_t v = __shfl_sync(kFull, mine, src);
+            const uint32_t off = (v ^ lane4) & 0xFFFFu;
+            PMS_CHECK(off < 4u * kTWords && off >= (B::X ? 4096u : 0u));
+            const uint32_t av = *reinterpret_cast<const uint32_t*>(Tb + off);
+            if (B::X == 0) {
+                acc[0] |= av;
+            } else {
+                common |= *reinterpret_cast<const uint32_t*>(Tb + off - 4096);
+                atomicOr(&wmask[lane * B::KW + (v >> 16)], av);
+            }
+        }
+    }
+    __syncwarp();
+    if (B::KW == 4) {
+        uint4* wv = reinterpret_cast<uint4*>(wmask + lane * 4);
+        const uint4 m = *wv;
+        *wv = make_uint4(0u, 0u, 0u, 0u);
+        acc[0] |= m.x | common;
+        acc[B::KW > 1 ? 1 : 0] |= m.y | common;
+        acc[B::KW > 2 ? 2 : 0] |= m.z | common;
+        acc[B::KW > 3 ? 3 : 0] |= m.w | common;
+    } else {
+#pragma unroll
+        for (int k = 0; k < B::KW; ++k) {
+            acc[k] |= wmask[lane * B::KW + k] | common;
+            wmask[lane * B::KW + k] = 0u;
+        }
+    }
+    __syncwarp();
+}
+
 // NW > 0: rows are padded to 32*NW windows and the window loops are fully
 // unrolled; NW = 0: any row length, 32 windows per lane per chunk.
 template <class P, int S, bool SMEM, int NW>
@@ -417,6 +499,10 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
     if (SMEM) mbar_wait(&bar, 0);
     const word* tab = SMEM ? tsm : static_cast<const word*>(a.tab);
     const int lane = threadIdx.x & 31;
+    // per-warp hit queue (NW > 0): 32*NW window indices after the tables
+    uint16_t* queue = reinterpret_cast<uint16_t*>(
+        reinterpret_cast<char*>(stab) + kTWords * 4 + (SMEM ? a.tab_bytes : 0u)) +
+        (threadIdx.x >> 5) * 32 * (NW > 0 ? NW : 1);
     unsigned long long scanned = 0, bscans = 0;
     const uint32_t dp1 = a.dp + 1u;
 
@@ -469,7 +555,10 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                                              hm, 1);
                     }
                     // pass 2: resolve the hits into each lane's candidate words
-                    drain_hits<P, S>(hm, NW - 1, row, a.Wp, cb, a.dp, lane, T, wmask, acc);
+                    if (PMS_QUEUE_DRAIN)
+                        drain_queue<P, S>(hm, NW - 1, row, queue, cb, a.dp, lane, T, wmask, acc);
+                    else
+                        drain_hits<P, S>(hm, NW - 1, row, a.Wp, cb, a.dp, lane, T, wmask, acc);
                 } else {
                     for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
                         uint32_t hm = 0;
