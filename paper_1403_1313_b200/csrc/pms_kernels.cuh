@@ -392,6 +392,9 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, int top, const typename 
     __syncwarp();
 }
 
+#ifndef PMS_R1_LOCAL
+#define PMS_R1_LOCAL 1
+#endif
 #ifndef PMS_QUEUE_DRAIN
 #define PMS_QUEUE_DRAIN 1
 #endif
@@ -434,6 +437,26 @@ __device__ __forceinline__ void drain_queue(uint32_t hm, int top, const typename
             if (p == dp) {
                 PMS_CHECK((((eH & 31u) << (2 * B::X)) | ek) < 32u * B::KW);
                 atomicOr(&wmask[((eH & 31u) << (2 * B::X)) | ek], 1u << (eL & 31u));
+            } else if (PMS_R1_LOCAL && p + 1u == dp) {
+                // r = 1: the radius-1 ball is small -- the finding lane ORs it in
+                // with 6 (S = 5) / 9 (S = 6) atomics instead of a warp broadcast:
+                // its own word with the five low positions flipped
+                // (T[1][eL & 31][0]), the five lanes with one H bit flipped
+                // (T[1][eL & 31][1 << j]), and (S = 6) the three other words of
+                // the upper position, centre bit only.
+                const uint32_t eh5 = eH & 31u, el5 = eL & 31u;
+                const uint32_t* T1 = T + 1024 + (el5 << 5);
+                uint32_t* wl = wmask + eh5 * B::KW;
+                atomicOr(wl + ek, T1[0]);
+#pragma unroll
+                for (int q = 0; q < 5; ++q)
+                    atomicOr(wmask + (eh5 ^ (1u << q)) * B::KW + ek, T1[1u << q]);
+                if (B::X) {
+                    const uint32_t bit = 1u << el5;
+                    atomicOr(wl + (ek ^ 1u), bit);
+                    atomicOr(wl + (ek ^ 2u), bit);
+                    atomicOr(wl + (ek ^ 3u), bit);
+                }
             } else {  // record: byte offset of T[r][eL & 31][eH & 31], word ek on top
                 const uint32_t r = min(dp - p, (uint32_t)(kTRows - 1));
                 mine = ((((r << 10) | ((eL & 31u) << 5) | (eH & 31u)) << 2)) | (ek << 16);
