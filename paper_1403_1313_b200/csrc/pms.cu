@@ -129,6 +129,9 @@ __global__ void __launch_bounds__(kBlock) pms_search_reg(SearchArgs a) {
 // ------------------------------------------------ block-family instances
 #define PMS_BLK5(nw) {5, nw, pms_search_block<Bp32, 5, true, nw>, pms_search_block<Bp32, 5, false, nw>},
 #define PMS_BLK6(nw) {6, nw, pms_search_block<Bp32, 6, true, nw>, pms_search_block<Bp32, 6, false, nw>},
+// per S: the generic (NW = 0) instance first, then register tiles ascending
+// (S = 7 -- 16 words per lane -- was measured slower: (15,4) 0.46-0.52 ms vs
+// 0.378, (16,5) 8.7-10.2 ms vs 4.8; its scans cost 4.7x an S = 6 scan)
 const BlockKernel kBlockKernels[] = {
     {5, 0, pms_search_block<Bp32, 5, true, 0>, pms_search_block<Bp32, 5, false, 0>},
     {6, 0, pms_search_block<Bp32, 6, true, 0>, pms_search_block<Bp32, 6, false, 0>},
@@ -306,7 +309,16 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         p->S = S;
     }
     p->tab_bytes = (uint32_t)((size_t)n * p->Wp * word_bytes);
-    const uint32_t static_smem = 12288;  // mbarrier, per-warp hit masks, slack
+    // static shared memory of the chosen kernel (mbarrier, per-warp hit masks)
+    uint32_t static_smem = 12288;
+    if (block_algo) {
+        cudaFuncAttributes fb{};
+        if (cudaFuncGetAttributes(&fb, (const void*)bk->fn_smem) != cudaSuccess) {
+            destroy_plan(p);
+            return fail_cuda(__LINE__);
+        }
+        static_smem = (uint32_t)fb.sharedSizeBytes;
+    }
     const uint32_t ball_bytes =
         block_algo ? (uint32_t)kTWords * 4u : 0u;  // ball table (28 KB)
     // block family with a register tile: per-warp hit queue (u16 window

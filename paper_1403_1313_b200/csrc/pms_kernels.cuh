@@ -58,6 +58,10 @@ constexpr int kBlkMinL = 5;        // the block family needs l >= 5
 // register-resident copy (38 registers at NW = 19) forced the drain loop to
 // rematerialise addresses under the 64-register cap (measured at (15,4):
 // 0.563 ms with it, 0.520 ms without).
+// Block family, register-tile path: balanced (queue) hit drain
+#ifndef PMS_QUEUE_DRAIN
+#define PMS_QUEUE_DRAIN 1
+#endif
 #ifndef PMS_BLK_MIN_CTAS
 #define PMS_BLK_MIN_CTAS 2
 #endif
@@ -299,7 +303,7 @@ template <int S>
 struct BlkTraits {
     static constexpr int X = S - 5;
     static constexpr int C = 1 << (2 * S);               // candidates per block
-    static constexpr int KW = 1 << (2 * X);              // mask words per lane
+    static constexpr int KW = 1 << (2 * X);              // mask words per lane (1, 4, 16)
     static constexpr uint32_t M = (1u << S) - 1u;        // suffix plane mask
 };
 constexpr int kTRows = 7;                                // rho = 0..6 (5, 6: all ones)
@@ -324,93 +328,143 @@ __device__ __forceinline__ uint32_t blk_sfx(uint32_t lane, uint32_t k, uint32_t 
     return P::template sfx_code<S>(lane | ((k >> X) << 5), b | ((k & ((1u << X) - 1u)) << 5));
 }
 
-// Process every pending hit of every lane and OR the matching candidates into
-// the lane's acc words.  Bit q of hm marks window row[lane + 32 * (top - q)]
-// (pass 1 shifts hit flags in from the bottom).
+// ---- hit resolution (pass 2), shared by both drains ----------------------
+// Words of the upper suffix positions (X of them) that differ from a hit's
+// word ek in exactly one position: ek ^ kUp1[u] (X = 1: 3 words, X = 2: 6).
+__device__ __forceinline__ uint32_t up1_delta(int X, int u) {
+    // u = 3*pos + alt; alt 0: L bit, 1: H bit, 2: both
+    const uint32_t pos = (uint32_t)u / 3u, alt = (uint32_t)u % 3u;
+    const uint32_t lb = 1u << pos, hb = 1u << (X + pos);
+    return alt == 0 ? lb : alt == 1 ? hb : (lb | hb);
+}
+
+// One hit (window w with prefix distance p <= d) of the finding lane:
+//   r = 0: one atomic OR (the window's own suffix);
+//   r = 1: the radius-1 ball, ORed by this lane with 6 + 3X atomics: its own
+//          word with the five low positions flipped (T[1][eL & 31][0]), the
+//          five lanes with one H bit flipped (T[1][eL & 31][1 << q]), and the
+//          3X words one upper position away (centre bit only);
+//   r >= 2: returns a broadcast record (byte offset of T[r][eL & 31][eH & 31],
+//          word ek on top), else kFull.
 template <class P, int S>
-__device__ __forceinline__ void drain_hits(uint32_t hm, int top, const typename P::word* row,
-                                           int wp, uint2 cb, uint32_t dp, int lane,
-                                           const uint32_t* T, uint32_t* wmask,
-                                           uint32_t (&acc)[BlkTraits<S>::KW]) {
-    (void)wp;  // row length (windows), used by the debug bounds checks
+__device__ __forceinline__ uint32_t resolve_hit(typename P::word w, uint2 cb, uint32_t dp,
+                                                const uint32_t* T, uint32_t* wmask) {
+    using B = BlkTraits<S>;
+    const uint32_t p = P::template prefix_dist<S>(cb, w);
+    const uint32_t eH = P::template sfx_h<S>(w), eL = P::template sfx_l<S>(w);
+    const uint32_t ek = ((eH >> 5) << B::X) | (eL >> 5);  // word of w's upper positions
+    const uint32_t eh5 = eH & 31u, el5 = eL & 31u;
+    uint32_t* wl = wmask + eh5 * B::KW;                    // lane eh5's words
+    if (p == dp) {
+        PMS_CHECK(eh5 * B::KW + ek < 32u * B::KW);
+        atomicOr(wl + ek, 1u << el5);
+        return kFull;
+    }
+    if (p + 1u == dp) {
+        const uint32_t* T1 = T + 1024 + (el5 << 5);
+        atomicOr(wl + ek, T1[0]);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) atomicOr(wmask + (eh5 ^ (1u << q)) * B::KW + ek, T1[1u << q]);
+#pragma unroll
+        for (int u = 0; u < 3 * B::X; ++u) atomicOr(wl + (ek ^ up1_delta(B::X, u)), 1u << el5);
+        return kFull;
+    }
+    const uint32_t r = min(dp - p, (uint32_t)(kTRows - 1));
+    return (((r << 10) | (el5 << 5) | eh5) << 2) | (ek << 16);
+}
+
+// Apply every broadcast record of the warp (one SHFL each): per lane, word ek
+// gets T[r] (A), the words one upper position away T[r-1] (B), and -- as
+// `common`, which every word receives at the end of the scan -- the row for
+// all X upper positions mismatched, T[r-X].  X = 0: A only.
+template <int S>
+__device__ __forceinline__ void apply_broadcasts(uint32_t mine, int lane, const uint32_t* T,
+                                                 uint32_t* wmask, uint32_t& common) {
     using B = BlkTraits<S>;
     const char* Tb = reinterpret_cast<const char*>(T);
     const uint32_t lane4 = (uint32_t)lane << 2;
-    uint32_t common = 0u;  // ball words with one upper-position mismatch (all words)
+    uint32_t who = __ballot_sync(kFull, mine != kFull);
+    while (who) {
+        const int src = msb(who);
+        who &= ~(1u << src);
+        const uint32_t v = __shfl_sync(kFull, mine, src);
+        const uint32_t off = (v ^ lane4) & 0xFFFFu;
+        PMS_CHECK(off < 4u * kTWords && off >= 4096u * B::X);
+        const uint32_t a = *reinterpret_cast<const uint32_t*>(Tb + off);
+        uint32_t* wl = wmask + lane * B::KW;
+        const uint32_t ek = v >> 16;
+        atomicOr(wl + ek, a);  // the lane's own word: conflict-free
+        if (B::X > 0) {
+            common |= *reinterpret_cast<const uint32_t*>(Tb + off - 4096 * B::X);
+            if (B::X > 1) {
+                const uint32_t b = *reinterpret_cast<const uint32_t*>(Tb + off - 4096);
+#pragma unroll
+                for (int u = 0; u < 3 * B::X; ++u) atomicOr(wl + (ek ^ up1_delta(B::X, u)), b);
+            }
+        }
+    }
+}
+
+// End of a (block, sequence) scan: alive &= (the lane's words | common); the
+// words are cleared for the next scan.  Returns this lane's "any alive".
+template <int S>
+__device__ __forceinline__ uint32_t finish_scan(uint32_t* wmask, int lane, uint32_t common,
+                                                uint32_t (&alive)[BlkTraits<S>::KW]) {
+    using B = BlkTraits<S>;
+    __syncwarp();
+    uint32_t any = 0u;
+    if (B::KW % 4 == 0) {  // 16-B accesses
+        uint4* wv = reinterpret_cast<uint4*>(wmask + lane * B::KW);
+#pragma unroll
+        for (int q = 0; q < B::KW / 4; ++q) {
+            const uint4 m = wv[q];
+            wv[q] = make_uint4(0u, 0u, 0u, 0u);
+            alive[(4 * q + 0) % B::KW] &= m.x | common;
+            alive[(4 * q + 1) % B::KW] &= m.y | common;
+            alive[(4 * q + 2) % B::KW] &= m.z | common;
+            alive[(4 * q + 3) % B::KW] &= m.w | common;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < B::KW; ++k) {
+            alive[k] &= wmask[lane * B::KW + k] | common;
+            wmask[lane * B::KW + k] = 0u;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < B::KW; ++k) any |= alive[k];
+    __syncwarp();
+    return any;
+}
+
+// Per-lane drain (NW = 0 streaming path): each lane resolves its own hits,
+// one per round (bit q of hm marks window row[lane + 32 * (top - q)]).
+template <class P, int S>
+__device__ __forceinline__ void drain_hits(uint32_t hm, int top, const typename P::word* row,
+                                           int wp, uint2 cb, uint32_t dp, int lane,
+                                           const uint32_t* T, uint32_t* wmask, uint32_t& common) {
+    (void)wp;
     while (__any_sync(kFull, hm != 0u)) {
         uint32_t mine = kFull;
         if (hm) {
             const int q = msb(hm);  // any order
             hm &= ~(1u << q);
             PMS_CHECK(lane + 32 * (top - q) < wp && top - q >= 0);
-            const typename P::word w = row[lane + 32 * (top - q)];
-            const uint32_t p = P::template prefix_dist<S>(cb, w);
-            const uint32_t eH = P::template sfx_h<S>(w), eL = P::template sfx_l<S>(w);
-            const uint32_t ek = ((eH >> 5) << B::X) | (eL >> 5);  // word of w's upper position
-            if (p == dp) {
-                PMS_CHECK((((eH & 31u) << (2 * B::X)) | ek) < 32u * B::KW);
-                atomicOr(&wmask[((eH & 31u) << (2 * B::X)) | ek], 1u << (eL & 31u));
-            } else {  // record: byte offset of T[r][eL & 31][eH & 31], word ek on top
-                const uint32_t r = min(dp - p, (uint32_t)(kTRows - 1));
-                mine = ((((r << 10) | ((eL & 31u) << 5) | (eH & 31u)) << 2)) | (ek << 16);
-            }
+            mine = resolve_hit<P, S>(row[lane + 32 * (top - q)], cb, dp, T, wmask);
         }
-        uint32_t who = __ballot_sync(kFull, mine != kFull);
-        while (who) {
-            const int src = msb(who);
-            who &= ~(1u << src);
-            const uint32_t v = __shfl_sync(kFull, mine, src);
-            const uint32_t off = (v ^ lane4) & 0xFFFFu;
-            PMS_CHECK(off < 4u * kTWords && off >= (B::X ? 4096u : 0u));
-            const uint32_t a = *reinterpret_cast<const uint32_t*>(Tb + off);
-            if (B::X == 0) {
-                acc[0] |= a;
-            } else {
-                common |= *reinterpret_cast<const uint32_t*>(Tb + off - 4096);
-                // A into the lane's own word ek of the shared mask: one
-                // conflict-free atomic instead of a branch tree over acc[k]
-                atomicOr(&wmask[lane * B::KW + (v >> 16)], a);
-            }
-        }
+        apply_broadcasts<S>(mine, lane, T, wmask, common);
     }
-    __syncwarp();
-    if (B::KW == 4) {  // the lane's four words in one 16-B access each way
-        uint4* wv = reinterpret_cast<uint4*>(wmask + lane * 4);
-        const uint4 m = *wv;
-        *wv = make_uint4(0u, 0u, 0u, 0u);
-        acc[0] |= m.x | common;
-        acc[B::KW > 1 ? 1 : 0] |= m.y | common;
-        acc[B::KW > 2 ? 2 : 0] |= m.z | common;
-        acc[B::KW > 3 ? 3 : 0] |= m.w | common;
-    } else {
-#pragma unroll
-        for (int k = 0; k < B::KW; ++k) {
-            acc[k] |= wmask[lane * B::KW + k] | common;
-            wmask[lane * B::KW + k] = 0u;
-        }
-    }
-    __syncwarp();
 }
 
-#ifndef PMS_R1_LOCAL
-#define PMS_R1_LOCAL 1
-#endif
-#ifndef PMS_QUEUE_DRAIN
-#define PMS_QUEUE_DRAIN 1
-#endif
 // Balanced drain (NW > 0): the warp's hits are first compacted into a
 // per-warp shared-memory queue of window indices (exclusive prefix sum of the
 // lanes' hit counts, then each lane writes its own), and the queue is
-// processed 32 hits per round -- typically ONE round, where the per-lane
-// drain needs max-over-lanes(hits) rounds of the same work.
+// processed 32 hits per round -- typically one or two rounds, where the
+// per-lane drain needs max-over-lanes(hits) rounds of the same work.
 template <class P, int S>
 __device__ __forceinline__ void drain_queue(uint32_t hm, int top, const typename P::word* row,
                                             uint16_t* queue, uint2 cb, uint32_t dp, int lane,
-                                            const uint32_t* T, uint32_t* wmask,
-                                            uint32_t (&acc)[BlkTraits<S>::KW]) {
-    using B = BlkTraits<S>;
-    const char* Tb = reinterpret_cast<const char*>(T);
-    const uint32_t lane4 = (uint32_t)lane << 2;
+                                            const uint32_t* T, uint32_t* wmask, uint32_t& common) {
     const uint32_t nh = __popc(hm);
     uint32_t inc = nh;  // inclusive prefix sum of the hit counts over lanes
 #pragma unroll
@@ -426,75 +480,11 @@ __device__ __forceinline__ void drain_queue(uint32_t hm, int top, const typename
         queue[pos++] = (uint16_t)(lane + 32 * (top - q));
     }
     __syncwarp();
-    uint32_t common = 0u;  // ball words with one upper-position mismatch (all words)
     for (uint32_t base = 0; base < total; base += 32) {
         uint32_t mine = kFull;
-        if (base + lane < total) {
-            const typename P::word w = row[queue[base + lane]];
-            const uint32_t p = P::template prefix_dist<S>(cb, w);
-            const uint32_t eH = P::template sfx_h<S>(w), eL = P::template sfx_l<S>(w);
-            const uint32_t ek = ((eH >> 5) << B::X) | (eL >> 5);  // word of w's upper position
-            if (p == dp) {
-                PMS_CHECK((((eH & 31u) << (2 * B::X)) | ek) < 32u * B::KW);
-                atomicOr(&wmask[((eH & 31u) << (2 * B::X)) | ek], 1u << (eL & 31u));
-            } else if (PMS_R1_LOCAL && p + 1u == dp) {
-                // r = 1: the radius-1 ball is small -- the finding lane ORs it in
-                // with 6 (S = 5) / 9 (S = 6) atomics instead of a warp broadcast:
-                // its own word with the five low positions flipped
-                // (T[1][eL & 31][0]), the five lanes with one H bit flipped
-                // (T[1][eL & 31][1 << j]), and (S = 6) the three other words of
-                // the upper position, centre bit only.
-                const uint32_t eh5 = eH & 31u, el5 = eL & 31u;
-                const uint32_t* T1 = T + 1024 + (el5 << 5);
-                uint32_t* wl = wmask + eh5 * B::KW;
-                atomicOr(wl + ek, T1[0]);
-#pragma unroll
-                for (int q = 0; q < 5; ++q)
-                    atomicOr(wmask + (eh5 ^ (1u << q)) * B::KW + ek, T1[1u << q]);
-                if (B::X) {
-                    const uint32_t bit = 1u << el5;
-                    atomicOr(wl + (ek ^ 1u), bit);
-                    atomicOr(wl + (ek ^ 2u), bit);
-                    atomicOr(wl + (ek ^ 3u), bit);
-                }
-            } else {  // record: byte offset of T[r][eL & 31][eH & 31], word ek on top
-                const uint32_t r = min(dp - p, (uint32_t)(kTRows - 1));
-                mine = ((((r << 10) | ((eL & 31u) << 5) | (eH & 31u)) << 2)) | (ek << 16);
-            }
-        }
-        uint32_t who = __ballot_sync(kFull, mine != kFull);
-        while (who) {
-            const int src = msb(who);
-            who &= ~(1u << src);
-            const uint32_t v = __shfl_sync(kFull, mine, src);
-            const uint32_t off = (v ^ lane4) & 0xFFFFu;
-            PMS_CHECK(off < 4u * kTWords && off >= (B::X ? 4096u : 0u));
-            const uint32_t av = *reinterpret_cast<const uint32_t*>(Tb + off);
-            if (B::X == 0) {
-                acc[0] |= av;
-            } else {
-                common |= *reinterpret_cast<const uint32_t*>(Tb + off - 4096);
-                atomicOr(&wmask[lane * B::KW + (v >> 16)], av);
-            }
-        }
+        if (base + lane < total) mine = resolve_hit<P, S>(row[queue[base + lane]], cb, dp, T, wmask);
+        apply_broadcasts<S>(mine, lane, T, wmask, common);
     }
-    __syncwarp();
-    if (B::KW == 4) {
-        uint4* wv = reinterpret_cast<uint4*>(wmask + lane * 4);
-        const uint4 m = *wv;
-        *wv = make_uint4(0u, 0u, 0u, 0u);
-        acc[0] |= m.x | common;
-        acc[B::KW > 1 ? 1 : 0] |= m.y | common;
-        acc[B::KW > 2 ? 2 : 0] |= m.z | common;
-        acc[B::KW > 3 ? 3 : 0] |= m.w | common;
-    } else {
-#pragma unroll
-        for (int k = 0; k < B::KW; ++k) {
-            acc[k] |= wmask[lane * B::KW + k] | common;
-            wmask[lane * B::KW + k] = 0u;
-        }
-    }
-    __syncwarp();
 }
 
 // NW > 0: rows are padded to 32*NW windows and the window loops are fully
@@ -563,9 +553,7 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                     if (__reduce_add_sync(kFull, na) <= a.handoff) break;
                 }
                 const word* row = tab + (size_t)i * a.Wp;
-                uint32_t acc[B::KW];
-#pragma unroll
-                for (int k = 0; k < B::KW; ++k) acc[k] = 0u;
+                uint32_t common = 0u;  // ball words every candidate word of the lane gets
                 // pass 1: prefix distance of each window; a hit (p <= d) makes
                 // p - (d + 1) negative, and its sign bit is shifted into hm
                 // (one funnel shift per window, no compare / select)
@@ -579,9 +567,9 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                     }
                     // pass 2: resolve the hits into each lane's candidate words
                     if (PMS_QUEUE_DRAIN)
-                        drain_queue<P, S>(hm, NW - 1, row, queue, cb, a.dp, lane, T, wmask, acc);
+                        drain_queue<P, S>(hm, NW - 1, row, queue, cb, a.dp, lane, T, wmask, common);
                     else
-                        drain_hits<P, S>(hm, NW - 1, row, a.Wp, cb, a.dp, lane, T, wmask, acc);
+                        drain_hits<P, S>(hm, NW - 1, row, a.Wp, cb, a.dp, lane, T, wmask, common);
                 } else {
                     for (int k0 = 0; k0 < a.Wp; k0 += 32 * 32) {  // 32 windows per lane per chunk
                         uint32_t hm = 0;
@@ -592,15 +580,10 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                                 P::template prefix_dist<S>(cb, row[k0 + lane + 32 * j]) - dp1, hm, 1);
                         }
                         drain_hits<P, S>(hm, nj - 1, row + k0, a.Wp - k0, cb, a.dp, lane, T, wmask,
-                                         acc);
+                                         common);
                     }
                 }
-                uint32_t any = 0;
-#pragma unroll
-                for (int k = 0; k < B::KW; ++k) {
-                    alive[k] &= acc[k];
-                    any |= alive[k];
-                }
+                const uint32_t any = finish_scan<S>(wmask, lane, common, alive);
                 ++bscans;
                 if (!__any_sync(kFull, any != 0u)) {  // skip rule for the whole block
                     dead = true;
