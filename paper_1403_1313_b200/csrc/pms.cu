@@ -221,8 +221,9 @@ struct pms_plan {
     pms_launch launch{};
     void* d_table = nullptr;        // packed windows [n][Wp]: uint32 (Bp32) or uint2 (Bp64)
     DevState* d_state = nullptr;
-    DevState* h_state = nullptr;  // pinned mirror, filled after each execution
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, packed, searched, state copied
+    DevState* h_state = nullptr;  // pinned mirror, read back by pms_plan_wait
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // start, packed, searched
+    cudaStream_t aux = nullptr;   // private stream for the state read-back
     SearchFn fn = nullptr;
     PackFn pack = nullptr;
     int wide = 0;                   // 64-bit window words (l > 16 or pms_launch.wide_words)
@@ -251,6 +252,7 @@ void destroy_plan(pms_plan* p) {
     cudaFreeHost(p->h_state);
     for (cudaEvent_t e : p->ev)
         if (e) cudaEventDestroy(e);
+    if (p->aux) cudaStreamDestroy(p->aux);
     delete p;
 }
 
@@ -400,6 +402,10 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
             destroy_plan(p);
             return fail_cuda(__LINE__);
         }
+    if (cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking) != cudaSuccess) {
+        destroy_plan(p);
+        return fail_cuda(__LINE__);
+    }
     *plan = p;
     return PMS_OK;
 }
@@ -448,13 +454,15 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     a.st = p->d_state; a.nout = reinterpret_cast<unsigned long long*>(d_count);
     a.out = d_out; a.out_wide = out_wide; a.cap = cap;
 
+    // device work of a step: state reset, pre-pass (which also zeroes the
+    // result counter), search; the state read-back is pms_plan_wait's
     if (cudaEventRecord(p->ev[0], s) != cudaSuccess) return fail_cuda(__LINE__);
-    if (cudaMemsetAsync(p->d_state, 0, sizeof(DevState), s) != cudaSuccess ||
-        cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s) != cudaSuccess)
+    if (cudaMemsetAsync(p->d_state, 0, sizeof(DevState), s) != cudaSuccess)
         return fail_cuda(__LINE__);
     const long long cells = (long long)p->n * p->Wp;
     p->pack<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(d_seqs, p->n, p->t, p->l, p->W, p->Wp,
-                                                             p->d_table, p->d_state);
+                                                             p->d_table, p->d_state,
+                                                             reinterpret_cast<unsigned long long*>(d_count));
     const cudaError_t e_pack = cudaGetLastError();
     if (e_pack != cudaSuccess) return fail_cuda(__LINE__, e_pack);
     if (cudaEventRecord(p->ev[1], s) != cudaSuccess) return fail_cuda(__LINE__);
@@ -464,10 +472,6 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
         if (e != cudaSuccess) return fail_cuda(__LINE__, e);
     }
     if (cudaEventRecord(p->ev[2], s) != cudaSuccess) return fail_cuda(__LINE__);
-    if (cudaMemcpyAsync(p->h_state, p->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s) !=
-        cudaSuccess)
-        return fail_cuda(__LINE__);
-    if (cudaEventRecord(p->ev[3], s) != cudaSuccess) return fail_cuda(__LINE__);
     p->executed = true;
     return PMS_OK;
 }
@@ -486,7 +490,12 @@ extern "C" int pms_plan_execute64(pms_plan* p, const uint8_t* d_seqs, uint64_t l
 
 extern "C" int pms_plan_wait(pms_plan* p, pms_stats* stats) {
     if (!p || !p->executed) return PMS_E_ARG;
-    if (cudaEventSynchronize(p->ev[3]) != cudaSuccess) return fail_cuda(__LINE__);
+    // read the state back on the plan's own stream once the search is done
+    if (cudaStreamWaitEvent(p->aux, p->ev[2], 0) != cudaSuccess ||
+        cudaMemcpyAsync(p->h_state, p->d_state, sizeof(DevState), cudaMemcpyDeviceToHost,
+                        p->aux) != cudaSuccess ||
+        cudaStreamSynchronize(p->aux) != cudaSuccess)
+        return fail_cuda(__LINE__);
     if (stats) {
         float pack = 0.f, search = 0.f, tot = 0.f;
         cudaEventElapsedTime(&pack, p->ev[0], p->ev[1]);

@@ -43,7 +43,8 @@ struct SearchArgs {
 };
 
 using SearchFn = void (*)(SearchArgs);
-using PackFn = void (*)(const uint8_t*, int, int, int, int, int, void*, DevState*);
+using PackFn = void (*)(const uint8_t*, int, int, int, int, int, void*, DevState*,
+                        unsigned long long*);
 
 struct BlockKernel {
     int S, NW;
@@ -154,11 +155,14 @@ using namespace pms;
 // are padded to Wp with copies of window W-1, which cannot change "some window
 // is within d".  Every byte lies in at least one window, so the byte check
 // covers the whole input.
+// Thread 0 also zeroes the caller's result counter (saves a memset launch).
 template <class P>
 __global__ void pms_pack_kernel(const uint8_t* __restrict__ seqs, int n, int t, int l, int W,
-                                int Wp, void* __restrict__ tab_, DevState* st) {
+                                int Wp, void* __restrict__ tab_, DevState* st,
+                                unsigned long long* nout) {
     typename P::word* tab = static_cast<typename P::word*>(tab_);
     const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx == 0) *nout = 0ull;
     if (idx >= (long long)n * Wp) return;
     const int i = (int)(idx / Wp);
     const int k = (int)(idx - (long long)i * Wp);
