@@ -132,7 +132,8 @@ typedef struct pms_stats {
  * An empty result is PMS_OK with *count = 0; d >= l yields all 4^l codes.
  * Steps: validate arguments -> H2D copy -> device pre-pass (byte check +
  * window packing) -> persistent search kernel with in-kernel atomic-append
- * compaction -> D2H of the count and codes -> host sort.
+ * compaction -> D2H of the state, the count and the first min(max_out, 1024)
+ * codes in one round trip (the rest only if the set is larger) -> host sort.
  * ------------------------------------------------------------------- */
 int pms_find(const uint8_t *seqs, int32_t n, int32_t t, int32_t l, int32_t d,
              uint32_t *out_codes, uint64_t max_out, uint64_t *count);

@@ -488,6 +488,43 @@ extern "C" int pms_plan_execute64(pms_plan* p, const uint8_t* d_seqs, uint64_t l
     return plan_execute(p, d_seqs, lo, hi, d_out, 1, cap, d_count, stream);
 }
 
+namespace {
+
+// Fill *stats from the plan's events and its (already read back) state.
+void fill_stats(pms_plan* p, pms_stats* stats) {
+    float pack = 0.f, search = 0.f, tot = 0.f;
+    cudaEventElapsedTime(&pack, p->ev[0], p->ev[1]);
+    cudaEventElapsedTime(&search, p->ev[1], p->ev[2]);
+    cudaEventElapsedTime(&tot, p->ev[0], p->ev[2]);
+    stats->pack_ms = pack;
+    stats->search_ms = search;
+    stats->total_ms = tot;
+    const unsigned long long cands = p->last_hi - p->last_lo;
+    stats->candidates = cands;
+    const unsigned long long W = (unsigned long long)p->W;
+    // candidate family: W compares per candidate on sequence 0 (register
+    // path) + W per further sequence scanned.  Block family: W prefix
+    // compares per (block, sequence) scan + W per per-candidate scan.
+    const bool seq0_implicit = !p->generic && p->algo == PMS_ALGO_CANDIDATE;
+    stats->issued_compares =
+        p->h_state->bad ? 0
+                        : (seq0_implicit ? cands * W : 0) +
+                              (p->h_state->extra + p->h_state->block_scans) * W;
+    stats->algo = p->algo;
+    stats->block_scans = p->h_state->block_scans;
+    stats->block_digits = p->S;
+    stats->motifs = 0;
+    stats->grid = p->grid;
+    stats->block = p->block;
+    stats->lanes_per_cand = p->G;
+    stats->windows_per_lane = p->NW;
+    stats->generic = p->generic;
+    stats->table_in_smem = p->in_smem;
+    stats->smem_bytes = p->smem_bytes;
+}
+
+}  // namespace
+
 extern "C" int pms_plan_wait(pms_plan* p, pms_stats* stats) {
     if (!p || !p->executed) return PMS_E_ARG;
     // read the state back on the plan's own stream once the search is done
@@ -496,37 +533,7 @@ extern "C" int pms_plan_wait(pms_plan* p, pms_stats* stats) {
                         p->aux) != cudaSuccess ||
         cudaStreamSynchronize(p->aux) != cudaSuccess)
         return fail_cuda(__LINE__);
-    if (stats) {
-        float pack = 0.f, search = 0.f, tot = 0.f;
-        cudaEventElapsedTime(&pack, p->ev[0], p->ev[1]);
-        cudaEventElapsedTime(&search, p->ev[1], p->ev[2]);
-        cudaEventElapsedTime(&tot, p->ev[0], p->ev[2]);
-        stats->pack_ms = pack;
-        stats->search_ms = search;
-        stats->total_ms = tot;
-        const unsigned long long cands = p->last_hi - p->last_lo;
-        stats->candidates = cands;
-        const unsigned long long W = (unsigned long long)p->W;
-        // candidate family: W compares per candidate on sequence 0 (register
-        // path) + W per further sequence scanned.  Block family: W prefix
-        // compares per (block, sequence) scan + W per per-candidate scan.
-        const bool seq0_implicit = !p->generic && p->algo == PMS_ALGO_CANDIDATE;
-        stats->issued_compares =
-            p->h_state->bad ? 0
-                            : (seq0_implicit ? cands * W : 0) +
-                                  (p->h_state->extra + p->h_state->block_scans) * W;
-        stats->algo = p->algo;
-        stats->block_scans = p->h_state->block_scans;
-        stats->block_digits = p->S;
-        stats->motifs = 0;
-        stats->grid = p->grid;
-        stats->block = p->block;
-        stats->lanes_per_cand = p->G;
-        stats->windows_per_lane = p->NW;
-        stats->generic = p->generic;
-        stats->table_in_smem = p->in_smem;
-        stats->smem_bytes = p->smem_bytes;
-    }
+    if (stats) fill_stats(p, stats);
     return p->h_state->bad ? PMS_E_CHAR : PMS_OK;
 }
 
@@ -569,6 +576,11 @@ struct CallCtx {
         if (stream) cudaStreamDestroy(stream);
     }
 };
+
+// codes copied back speculatively with the count (one host round trip when
+// the result set is small, as it is for planted-motif instances)
+constexpr unsigned long long kSpecCodes = 1024;
+static_assert(kSpecCodes * 8 <= (1ull << 19), "fits the pinned staging buffer");
 
 std::mutex g_pool_mu;
 std::vector<CallCtx*> g_pool;
@@ -679,32 +691,40 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
         healthy = false;
         return st;
     }
-    if (cudaMemcpyAsync(c->h_count, c->d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
-        cudaSuccess) {
+    // one round trip: state, count and (speculatively) the first codes come
+    // back with a single synchronisation; a second copy only for large sets
+    const unsigned long long spec = std::min<unsigned long long>(cap, kSpecCodes);
+    pms_plan* pl = c->plan;
+    if (cudaMemcpyAsync(pl->h_state, pl->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(c->h_count, c->d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        (spec > 0 && cudaMemcpyAsync(c->h_out, c->d_out, spec * sizeof(Code),
+                                     cudaMemcpyDeviceToHost, s) != cudaSuccess) ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
         healthy = false;
         return fail_cuda(__LINE__);
     }
-    st = pms_plan_wait(c->plan, stats);
-    if (cudaStreamSynchronize(s) != cudaSuccess) {
-        healthy = false;
-        return fail_cuda(__LINE__);
-    }
-    if (st == PMS_E_CUDA) healthy = false;
-    if (st != PMS_OK) return st;
+    if (stats) fill_stats(pl, stats);
+    if (pl->h_state->bad) return PMS_E_CHAR;
     const uint64_t found = *c->h_count;
     if (stats) stats->motifs = found;
     *count = found;
     if (found > max_out) return PMS_E_TRUNCATED;
     // a7: D2H of the codes, host sort (ascending code = lexicographic order)
     if (found > 0) {
-        const bool staged = found * sizeof(Code) <= CallCtx::kHostOutBytes;
-        if (cudaMemcpyAsync(staged ? c->h_out : (void*)out_codes, c->d_out, found * sizeof(Code),
-                            cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-            cudaStreamSynchronize(s) != cudaSuccess) {
-            healthy = false;
-            return fail_cuda(__LINE__);
+        if (found > spec) {
+            const bool staged = found * sizeof(Code) <= CallCtx::kHostOutBytes;
+            if (cudaMemcpyAsync(staged ? c->h_out : (void*)out_codes, c->d_out,
+                                found * sizeof(Code), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess) {
+                healthy = false;
+                return fail_cuda(__LINE__);
+            }
+            if (staged) std::memcpy(out_codes, c->h_out, found * sizeof(Code));
+        } else {
+            std::memcpy(out_codes, c->h_out, found * sizeof(Code));
         }
-        if (staged) std::memcpy(out_codes, c->h_out, found * sizeof(Code));
         std::sort(out_codes, out_codes + found);
     }
     return PMS_OK;
