@@ -198,6 +198,36 @@ bool pick_reg_kernel(int W, int force_g, RegKernel* best) {
     return found;
 }
 
+// The ball table T[rho][e][m] (bit b set iff popc(m | (b ^ e)) <= rho over five
+// positions, rho = 0..kTRows-1): computed once per device on the host and
+// bulk-copied into each CTA's shared memory by the block kernels.
+std::mutex g_ball_mu;
+uint32_t* g_ball[64] = {nullptr};
+
+const uint32_t* ensure_ball_table(int dev) {
+    std::lock_guard<std::mutex> lk(g_ball_mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!g_ball[dev]) {
+        std::vector<uint32_t> h(kTWords);
+        for (int idx = 0; idx < kTWords; ++idx) {
+            const uint32_t m = idx & 31u, e = (idx >> 5) & 31u;
+            const int rho = idx >> 10;
+            uint32_t w = 0;
+            for (uint32_t b = 0; b < 32; ++b)
+                if (__builtin_popcount(m | (b ^ e)) <= rho) w |= 1u << b;
+            h[idx] = w;
+        }
+        uint32_t* d = nullptr;
+        if (cudaMalloc(&d, kTWords * 4) != cudaSuccess) return nullptr;
+        if (cudaMemcpy(d, h.data(), kTWords * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(d);
+            return nullptr;
+        }
+        g_ball[dev] = d;
+    }
+    return g_ball[dev];
+}
+
 int ensure_constants() {
     static thread_local int dev_done[64] = {0};
     int dev = 0;
@@ -220,6 +250,7 @@ struct pms_plan {
     int dev = 0, sms = 0;
     pms_launch launch{};
     void* d_table = nullptr;        // packed windows [n][Wp]: uint32 (Bp32) or uint2 (Bp64)
+    const uint32_t* d_ball = nullptr;  // the device's ball table (block family; not owned)
     DevState* d_state = nullptr;
     DevState* h_state = nullptr;  // pinned mirror, read back by pms_plan_wait
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // start, packed, searched
@@ -336,6 +367,10 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         2u * (p->tab_bytes + ball_bytes + queue_bytes + static_smem + 1024u) > 233472u)
         p->in_smem = 0;
     p->smem_bytes = ball_bytes + (p->in_smem ? p->tab_bytes : 0) + queue_bytes;
+    if (block_algo && !(p->d_ball = ensure_ball_table(p->dev))) {
+        destroy_plan(p);
+        return fail_cuda(__LINE__);
+    }
 
     RegKernel rk{};
     const int force_g = (p->launch.lanes_per_cand == 16 || p->launch.lanes_per_cand == 32)
@@ -453,6 +488,7 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     a.handoff = p->launch.handoff > 0 ? p->launch.handoff : (p->d >= 5 ? 2 : 1);  // measured
     a.st = p->d_state; a.nout = reinterpret_cast<unsigned long long*>(d_count);
     a.out = d_out; a.out_wide = out_wide; a.cap = cap;
+    a.ball = p->d_ball;
 
     // device work of a step: state reset, pre-pass (which also zeroes the
     // result counter), search; the state read-back is pms_plan_wait's

@@ -36,6 +36,7 @@ struct SearchArgs {
     int handoff;                    // block family: <= this many survivors -> per-candidate
     int out_wide;                   // 1 = result codes are uint64, 0 = uint32
     uint32_t tab_bytes;
+    const uint32_t* ball;           // the ball table T in global memory (built once per device)
     DevState* st;
     unsigned long long* nout;       // result counter (caller's d_count)
     void* out;                      // result buffer, capacity cap (uint32 or uint64)
@@ -313,17 +314,6 @@ struct BlkTraits {
 constexpr int kTRows = 7;                                // rho = 0..6 (5, 6: all ones)
 constexpr int kTWords = kTRows * 1024;                   // 28 KB ball table
 
-__device__ __forceinline__ void build_suffix_table(uint32_t* T) {
-    for (int idx = threadIdx.x; idx < kTWords; idx += blockDim.x) {
-        const uint32_t m = idx & 31u, e = (idx >> 5) & 31u;
-        const int rho = idx >> 10;
-        uint32_t word = 0;
-        for (uint32_t b = 0; b < 32; ++b)
-            if ((int)__popc(m | (b ^ e)) <= rho) word |= 1u << b;
-        T[idx] = word;
-    }
-}
-
 // Suffix code (S digits, big-endian base 4) of the block candidate at
 // (lane, word k, bit b).
 template <class P, int S>
@@ -519,14 +509,20 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
 #pragma unroll
     for (int k = 0; k < B::KW; ++k) wmask[widx<S>(threadIdx.x & 31, k)] = 0u;
     word* tsm = reinterpret_cast<word*>(stab + kTWords);  // 128-B aligned for the bulk copy
-    if (SMEM) {  // start the table's TMA bulk copy, build the suffix table meanwhile
-        if (threadIdx.x == 0) mbar_init(&bar, 1);
-        __syncthreads();
-        if (threadIdx.x == 0) issue_table_copy(a, tsm, &bar);
-    }
-    build_suffix_table(T);
+    // prologue: TMA bulk copies of the ball table (28 KB, precomputed once per
+    // device) and, when staged, the window table into shared memory
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
-    if (SMEM) mbar_wait(&bar, 0);
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&bar, kTWords * 4u + (SMEM ? a.tab_bytes : 0u));
+        tma_bulk_g2s(T, a.ball, kTWords * 4u, &bar);
+        if (SMEM)
+            for (uint32_t off = 0; off < a.tab_bytes; off += 65536u)
+                tma_bulk_g2s(reinterpret_cast<char*>(tsm) + off,
+                             static_cast<const char*>(a.tab) + off, min(65536u, a.tab_bytes - off),
+                             &bar);
+    }
+    mbar_wait(&bar, 0);
     const word* tab = SMEM ? tsm : static_cast<const word*>(a.tab);
     const int lane = threadIdx.x & 31;
     // per-warp hit queue (NW > 0): 32*NW window indices after the tables
