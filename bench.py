@@ -336,8 +336,14 @@ def run_gpu(args) -> int:
     traffic = None
     tp = os.path.join(ROOT, "profiles",
                       "block_kernel_traffic.json" if block_family else "search_kernel_traffic.json")
+    ncu_ctx = None
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        tj = json.load(open(tp))
+        traffic = tj.get("dram_bytes_per_launch")
+        if "issue_slots_busy_pct" in tj:  # committed ncu capture of the same kernel (context)
+            ncu_ctx = {k: tj[k] for k in ("issue_slots_busy_pct", "alu_pipe_pct", "xu_pipe_pct",
+                                          "lsu_pipe_pct", "warp_instructions_per_launch",
+                                          "source") if k in tj}
     if block_family:
         # one POPC per window test; a block-family test resolves up to 1024 candidates
         achieved = issued_rate
@@ -416,6 +422,7 @@ def run_gpu(args) -> int:
                      "popc_peak_basis": f"POPC {POPC_PER_CLK_SM}/clk/SM x {sms} SMs x "
                                         f"{sm_mhz:.0f} MHz (median SM clock in the timed "
                                         "region); one POPC per window test",
+                     "ncu_capture": ncu_ctx,
                      "r_mix_kernel_ms": rmix_block["search_kernel_ms"] if rmix_block else None,
                      "r_mix_candidate_loop": rm["compares_per_s"] / 1e9,
                      "r_mix_clocks": clk_rm.summary()},
