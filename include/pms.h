@@ -95,7 +95,7 @@ typedef struct pms_launch {
  *     window's last S digits match that window (a Hamming-ball bitmask).  Each candidate keeps
  *     PAPER.md:63's semantics: it is compared with the windows of sequence
  *     0, 1, ... and dropped at the first sequence with no window within d; the
- *     block is abandoned when no candidate is left (the skip rule on 1024
+ *     block is abandoned when no candidate is left (the skip rule on 4^S
  *     candidates at once).  Needs l >= 5 (else the candidate family runs).
  *   PMS_ALGO_AUTO (0): PMS_ALGO_BLOCK when l >= 5, else PMS_ALGO_CANDIDATE. */
 enum { PMS_ALGO_AUTO = 0, PMS_ALGO_CANDIDATE = 1, PMS_ALGO_BLOCK = 2 };
@@ -197,9 +197,12 @@ int pms_plan_execute64(pms_plan *plan, const uint8_t *d_seqs, uint64_t lo,
                        uint64_t hi, uint64_t *d_out, uint64_t cap,
                        uint64_t *d_count, void *stream);
 
-/* Waits for the plan's last execution; returns PMS_E_CHAR if the pre-pass
- * saw an invalid byte (the search then did no work and *d_count is 0),
- * PMS_E_CUDA on a device error, else PMS_OK.  Fills *stats if non-NULL. */
+/* Waits for the plan's last execution (its search work, on a private stream
+ * ordered after it; later work the caller enqueued on `stream` is not waited
+ * for) and reads the plan's device state back; returns PMS_E_CHAR if the
+ * pre-pass saw an invalid byte (the search then did no work and *d_count is
+ * 0), PMS_E_CUDA on a device error, else PMS_OK.  Fills *stats if non-NULL
+ * (stats->motifs is 0 here: the count is in the caller's d_count). */
 int pms_plan_wait(pms_plan *plan, pms_stats *stats);
 
 void pms_plan_destroy(pms_plan *plan);
