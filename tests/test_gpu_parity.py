@@ -485,3 +485,37 @@ def test_compaction_stress_16_6(orc):
         hi = lo + 40000
         want = orc.find(s, 16, 6, lo=lo, hi=hi).codes.tolist()
         assert [c for c in got if lo <= c < hi] == want
+
+
+# ------------------------------------------ metamorphic relations on the GPU
+
+def _digits_reversed(c: int, l: int) -> int:
+    r = 0
+    for _ in range(l):
+        r = r * 4 + (c & 3)
+        c >>= 2
+    return r
+
+
+def test_gpu_metamorphic_relations():
+    """Relations the result set must satisfy, checked on the GPU
+    path directly: permuting or duplicating sequences keeps the set; adding a
+    sequence gives a subset; complementing every base (b -> 3-b) maps each code
+    c to c ^ (4^l - 1); reversing every sequence reverses each code's digits;
+    the set grows monotonically with d."""
+    l, d = 11, 3
+    s, _ = fmgen.generate_fm(20, 600, l, d, 2)
+    base = set(gpu(s, l, d).codes.tolist())
+    rng = np.random.default_rng(7)
+    assert set(gpu(s[rng.permutation(20)], l, d).codes.tolist()) == base
+    assert set(gpu(np.vstack([s, s[3:5]]), l, d).codes.tolist()) == base
+    extra = fmgen.random_sequences(1, 600, 99)
+    assert set(gpu(np.vstack([s, extra]), l, d).codes.tolist()) <= base
+    comp = {ord("A"): ord("T"), ord("C"): ord("G"), ord("G"): ord("C"), ord("T"): ord("A")}
+    sc = np.vectorize(comp.get)(s).astype(np.uint8)
+    mask = 4 ** l - 1
+    assert set(gpu(sc, l, d).codes.tolist()) == {c ^ mask for c in base}
+    sr = np.ascontiguousarray(s[:, ::-1])
+    assert set(gpu(sr, l, d).codes.tolist()) == {_digits_reversed(c, l) for c in base}
+    assert base <= set(gpu(s, l, d + 1).codes.tolist())
+    assert set(gpu(s, l, d - 1).codes.tolist()) <= base
