@@ -279,10 +279,10 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
 // w[l-S..l)), so one XOR / OR-fold / POPC of the prefix against w gives p,
 // and the block candidates that match w (distance <= d) are
 // exactly the suffixes within Hamming distance d - p of w's suffix.  After a
-// sequence, alive &= acc (the candidates with a window within d in it); the
+// sequence, alive &= (the candidates with a window within d in it); the
 // block is abandoned at the first sequence that leaves no candidate alive --
-// the skip rule on 4^S candidates at once -- and a lone survivor is finished
-// by the whole warp (check_sequences).
+// the skip rule on 4^S candidates at once -- and at most `handoff` survivors
+// are finished one by one by the whole warp (check_sequences).
 //
 // Candidates are indexed in BIT-PLANE order.  A suffix has planes (H, L) of S
 // bits (H = high bits, L = low bits of its base codes, position l-S in bit
@@ -292,18 +292,21 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
 //   lane = H & 31, bit = L & 31, word k = (H >> 5) << X | (L >> 5)  (X = S - 5,
 //   4^X words per lane).
 // A hit (window w, prefix distance p <= d, budget r = d - p) matches the
-// block candidates within distance r of w's suffix (eH, eL):
-//   * r = 0 (~80 % of hits) matches only the window's own suffix: the finding
-//     lane sets bit eL & 31 of word k(eH, eL) of lane eH & 31 in the warp's
-//     shared-memory mask (one atomic OR);
-//   * r >= 1: the hit is broadcast (one SHFL) and every lane reads two ball
-//     words of a table T[rho][e][m] (bit b set iff popc(m | (b ^ e)) <= rho,
-//     five positions): A = T[r][eL & 31][lane ^ (eH & 31)] for the word whose
-//     upper position matches w's, B = T[r-1][...] for the other words (one
-//     mismatch spent there).  B is the same for all of a lane's words, so it
-//     goes into one `common` register; A into the one matching word (an
-//     atomic OR on the lane's own word of the shared mask).  m is the
-//     fastest index: a broadcast reads 32 distinct banks.
+// block candidates within distance r of w's suffix (eH, eL); pass 2
+// (drain_queue / resolve_hit / apply_broadcasts below) ORs them into the
+// warp's shared-memory words:
+//   * r = 0 (~80 % of hits): only the window's own suffix -- one atomic OR of
+//     bit eL & 31 into word k(eH, eL) of lane eH & 31;
+//   * r = 1 (~18 %): the radius-1 ball, ORed by the finding lane itself with
+//     6 + 3X atomics (ball-table rows, below);
+//   * r >= 2: broadcast (one SHFL) to all lanes, which read two words of the
+//     ball table T[rho][e][m] (bit b set iff popc(m | (b ^ e)) <= rho, five
+//     positions): A = T[r][eL & 31][lane ^ (eH & 31)] for the word whose upper
+//     position matches w's, B = T[r-1][...] for the other words (one mismatch
+//     spent there).  B is the same for all of a lane's words, so it goes into
+//     one `common` register; A into the one matching word (an atomic OR on
+//     the lane's own word).  m is the fastest index: a broadcast reads 32
+//     distinct banks.
 template <int S>
 struct BlkTraits {
     static constexpr int X = S - 5;
