@@ -53,7 +53,10 @@ struct BlockKernel {
 };
 
 constexpr int kBlock = 256;        // threads per CTA of the candidate family (8 warps)
-constexpr int kBlockB = 512;       // max threads per CTA of the block family
+#ifndef PMS_BLK_MAX_THREADS
+#define PMS_BLK_MAX_THREADS 512
+#endif
+constexpr int kBlockB = PMS_BLK_MAX_THREADS;  // max threads per CTA of the block family
 constexpr int kUnitMax = 4096;     // largest block (S = 6)
 constexpr int kBlkMinL = 5;        // the block family needs l >= 5
 // Sequence 0 streams from shared memory like the other sequences: a
