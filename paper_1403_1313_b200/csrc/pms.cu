@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -595,6 +596,15 @@ struct CallCtx {
     void* h_out = nullptr;        // pinned staging of small result sets
     static constexpr unsigned long long kHostOutBytes = 1ull << 19;
     cudaStream_t stream = nullptr;
+    // the call's device work (H2D, pre-pass, search, D2H) as one CUDA graph,
+    // re-captured when the range, capacity, code width or buffers change
+    cudaGraphExec_t gexec = nullptr;
+    unsigned long long g_lo = 0, g_hi = 0, g_cap = 0;
+    int g_wide = -1, g_disabled = 0;
+    void* g_out = nullptr;
+    // previous call's parameters: a graph is captured only for a repeat
+    unsigned long long p_lo = ~0ull, p_hi = 0, p_cap = 0;
+    int p_wide = -1;
 
     bool matches(int dv, int32_t n_, int32_t t_, int32_t l_, int32_t d_,
                  const pms_launch& L) const {
@@ -602,6 +612,7 @@ struct CallCtx {
                std::memcmp(&launch, &L, sizeof(L)) == 0;
     }
     void release_resources() {
+        if (gexec) cudaGraphExecDestroy(gexec);
         destroy_plan(plan);
         cudaFree(d_seqs);
         cudaFree(d_out);
@@ -717,27 +728,72 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
     }
     cudaStream_t s = c->stream;
     std::memcpy(c->h_seqs, seqs, (size_t)n * t);  // pinned staging: the H2D is a true async DMA
-    if (cudaMemcpyAsync(c->d_seqs, c->h_seqs, (size_t)n * t, cudaMemcpyHostToDevice, s) !=
-        cudaSuccess) {
-        healthy = false;
-        return fail_cuda(__LINE__);
-    }
-    st = plan_execute(c->plan, c->d_seqs, lo, hi, c->d_out, kWide, cap, c->d_count, s);
-    if (st != PMS_OK) {
-        healthy = false;
-        return st;
-    }
     // one round trip: state, count and (speculatively) the first codes come
     // back with a single synchronisation; a second copy only for large sets
     const unsigned long long spec = std::min<unsigned long long>(cap, kSpecCodes);
     pms_plan* pl = c->plan;
-    if (cudaMemcpyAsync(pl->h_state, pl->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s) !=
-            cudaSuccess ||
-        cudaMemcpyAsync(c->h_count, c->d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
-            cudaSuccess ||
-        (spec > 0 && cudaMemcpyAsync(c->h_out, c->d_out, spec * sizeof(Code),
-                                     cudaMemcpyDeviceToHost, s) != cudaSuccess) ||
-        cudaStreamSynchronize(s) != cudaSuccess) {
+    // the call's device work: H2D, pre-pass + search (plan_execute), D2H
+    auto enqueue = [&]() -> int {
+        if (cudaMemcpyAsync(c->d_seqs, c->h_seqs, (size_t)n * t, cudaMemcpyHostToDevice, s) !=
+            cudaSuccess)
+            return fail_cuda(__LINE__);
+        const int e = plan_execute(pl, c->d_seqs, lo, hi, c->d_out, kWide, cap, c->d_count, s);
+        if (e != PMS_OK) return e;
+        if (cudaMemcpyAsync(pl->h_state, pl->d_state, sizeof(DevState), cudaMemcpyDeviceToHost,
+                            s) != cudaSuccess ||
+            cudaMemcpyAsync(c->h_count, c->d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
+                cudaSuccess ||
+            (spec > 0 && cudaMemcpyAsync(c->h_out, c->d_out, spec * sizeof(Code),
+                                         cudaMemcpyDeviceToHost, s) != cudaSuccess))
+            return fail_cuda(__LINE__);
+        return PMS_OK;
+    };
+    // replayed as a CUDA graph (one launch instead of ~8 API calls) unless
+    // PMS_NO_GRAPH is set or capture is unavailable
+    static const bool no_graph = std::getenv("PMS_NO_GRAPH") != nullptr;
+    bool graphed = false;
+    const bool repeat = c->p_lo == lo && c->p_hi == hi && c->p_cap == cap && c->p_wide == kWide;
+    c->p_lo = lo; c->p_hi = hi; c->p_cap = cap; c->p_wide = kWide;
+    const bool have = c->gexec && c->g_lo == lo && c->g_hi == hi && c->g_cap == cap &&
+                      c->g_wide == kWide && c->g_out == c->d_out;
+    if (!no_graph && !c->g_disabled && (have || repeat)) {
+        if (!have) {
+            if (c->gexec) cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+            cudaGraph_t g = nullptr;
+            if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                const int e = enqueue();
+                const cudaError_t ee = cudaStreamEndCapture(s, &g);
+                if (e == PMS_OK && ee == cudaSuccess && g &&
+                    cudaGraphInstantiate(&c->gexec, g, 0) == cudaSuccess) {
+                    c->g_lo = lo; c->g_hi = hi; c->g_cap = cap; c->g_wide = kWide;
+                    c->g_out = c->d_out;
+                } else {
+                    c->gexec = nullptr;
+                    c->g_disabled = 1;
+                }
+                if (g) cudaGraphDestroy(g);
+            } else {
+                c->g_disabled = 1;
+            }
+            cudaGetLastError();  // clear a failed capture's error state
+        }
+        if (c->gexec) {
+            if (cudaGraphLaunch(c->gexec, s) != cudaSuccess) {
+                healthy = false;
+                return fail_cuda(__LINE__);
+            }
+            graphed = true;
+        }
+    }
+    if (!graphed) {
+        st = enqueue();
+        if (st != PMS_OK) {
+            healthy = false;
+            return st;
+        }
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
         healthy = false;
         return fail_cuda(__LINE__);
     }
