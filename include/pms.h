@@ -134,9 +134,9 @@ typedef struct pms_stats {
  * window packing) -> persistent search kernel with in-kernel atomic-append
  * compaction -> D2H of the state, the count and the first min(max_out, 1024)
  * codes in one round trip (the rest only if the set is larger) -> host sort.
- * A call that repeats the previous call's shape, range and capacity (same
- * pooled context) replays the device work as one CUDA graph; set the
- * environment variable PMS_NO_GRAPH to always enqueue it call by call.
+ * A call without stats that repeats the previous call's shape, range and
+ * capacity (same pooled context) replays the device work as one CUDA graph;
+ * set the environment variable PMS_NO_GRAPH to always enqueue it call by call.
  * ------------------------------------------------------------------- */
 int pms_find(const uint8_t *seqs, int32_t n, int32_t t, int32_t l, int32_t d,
              uint32_t *out_codes, uint64_t max_out, uint64_t *count);

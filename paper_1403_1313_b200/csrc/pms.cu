@@ -756,7 +756,9 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
     c->p_lo = lo; c->p_hi = hi; c->p_cap = cap; c->p_wide = kWide;
     const bool have = c->gexec && c->g_lo == lo && c->g_hi == hi && c->g_cap == cap &&
                       c->g_wide == kWide && c->g_out == c->d_out;
-    if (!no_graph && !c->g_disabled && (have || repeat)) {
+    // (not when stats are requested: the per-kernel event timings stay those of
+    // an ordinary enqueue)
+    if (!no_graph && !stats && !c->g_disabled && (have || repeat)) {
         if (!have) {
             if (c->gexec) cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
