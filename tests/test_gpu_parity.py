@@ -519,3 +519,27 @@ def test_gpu_metamorphic_relations():
     assert set(gpu(sr, l, d).codes.tolist()) == {_digits_reversed(c, l) for c in base}
     assert base <= set(gpu(s, l, d + 1).codes.tolist())
     assert set(gpu(s, l, d - 1).codes.tolist()) <= base
+
+
+def test_graph_replay_sees_new_inputs(orc):
+    """Repeated calls with the same shape, range and capacity replay the
+    device work as a CUDA graph (include/pms.h); each call must still search
+    its own input: alternate two inputs of one shape and compare with the
+    oracle every time (with and without stats, and after a range change)."""
+    a, _ = fmgen.generate_fm(10, 120, 9, 2, 501)
+    b, _ = fmgen.generate_fm(10, 120, 9, 2, 502)
+    want = {id(a): orc.find(a, 9, 2).codes.tolist(), id(b): orc.find(b, 9, 2).codes.tolist()}
+    assert want[id(a)] != want[id(b)]
+    for k in range(8):
+        s = a if k % 2 == 0 else b
+        r = pms.find_ex(s, 9, 2, want_stats=(k == 5))
+        assert r.status == 0 and r.codes.tolist() == want[id(s)], k
+    r = pms.find_ex(a, 9, 2, lo=1000, hi=90000, want_stats=False)
+    assert r.codes.tolist() == orc.find(a, 9, 2, lo=1000, hi=90000).codes.tolist()
+    r = pms.find_ex(b, 9, 2, lo=1000, hi=90000, want_stats=False)
+    assert r.codes.tolist() == orc.find(b, 9, 2, lo=1000, hi=90000).codes.tolist()
+    bad = a.copy()
+    bad[0, 0] = ord("N")
+    assert pms.find_ex(bad, 9, 2, lo=1000, hi=90000, want_stats=False).status == pms.E_CHAR
+    assert pms.find_ex(b, 9, 2, lo=1000, hi=90000, want_stats=False).codes.tolist() == \
+        orc.find(b, 9, 2, lo=1000, hi=90000).codes.tolist()
