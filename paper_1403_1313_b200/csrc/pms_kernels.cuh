@@ -537,6 +537,13 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
         (threadIdx.x >> 5) * 32 * (NW > 0 ? NW : 1);
     unsigned long long scanned = 0, bscans = 0;
     const uint32_t dp1 = a.dp + 1u;
+    // register tile: hit bits of this lane's real windows (lane + 32j < W; the
+    // padding repeats window W-1 and would only re-deliver its hits)
+    uint32_t real = kFull;
+    if (NW > 0) {
+        const int nreal = min(NW, max(0, (a.W - lane + 31) / 32));
+        real = (nreal == 0) ? 0u : ((nreal >= 32 ? kFull : ((1u << nreal) - 1u)) << (NW - nreal));
+    }
 
     for (;;) {
         unsigned long long b = 0;
@@ -584,6 +591,7 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                         hm = __funnelshift_l(P::template prefix_dist<S>(cb, row[lane + 32 * j]) - dp1,
                                              hm, 1);
                     }
+                    hm &= real;
                     // pass 2: resolve the hits into each lane's candidate words
                     if (PMS_QUEUE_DRAIN)
                         drain_queue<P, S>(hm, NW - 1, row, queue, cb, a.dp, lane, T, wmask, common);
