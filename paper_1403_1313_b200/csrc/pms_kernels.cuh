@@ -419,13 +419,12 @@ __device__ __forceinline__ void apply_broadcasts(uint32_t mine, int lane, const 
 }
 
 // End of a (block, sequence) scan: alive &= (the lane's words | common); the
-// words are cleared for the next scan.  Returns this lane's "any alive".
+// words are cleared for the next scan.
 template <int S>
-__device__ __forceinline__ uint32_t finish_scan(uint32_t* wmask, int lane, uint32_t common,
-                                                uint32_t (&alive)[BlkTraits<S>::KW]) {
+__device__ __forceinline__ void finish_scan(uint32_t* wmask, int lane, uint32_t common,
+                                            uint32_t (&alive)[BlkTraits<S>::KW]) {
     using B = BlkTraits<S>;
     __syncwarp();
-    uint32_t any = 0u;
     if (B::KW % 4 == 0 && !PMS_WMASK_KMAJOR) {  // lane-major: 16-B accesses
         uint4* wv = reinterpret_cast<uint4*>(wmask + lane * B::KW);
 #pragma unroll
@@ -444,10 +443,7 @@ __device__ __forceinline__ uint32_t finish_scan(uint32_t* wmask, int lane, uint3
             wmask[widx<S>(lane, k)] = 0u;
         }
     }
-#pragma unroll
-    for (int k = 0; k < B::KW; ++k) any |= alive[k];
     __syncwarp();
-    return any;
 }
 
 // Per-lane drain (NW = 0 streaming path): each lane resolves its own hits,
@@ -571,13 +567,9 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
             }
             int i = 0;
             bool dead = false;
+            int nalive = B::C;  // the block's alive candidates (warp total) after sequence i-1
             for (; i < a.n; ++i) {
-                if (i > 0 && a.skip) {
-                    int na = 0;
-#pragma unroll
-                    for (int k = 0; k < B::KW; ++k) na += __popc(alive[k]);
-                    if (__reduce_add_sync(kFull, na) <= a.handoff) break;
-                }
+                if (i > 0 && a.skip && nalive <= a.handoff) break;
                 const word* row = tab + (size_t)i * a.Wp;
                 uint32_t common = 0u;  // ball words every candidate word of the lane gets
                 // pass 1: prefix distance of each window; a hit (p <= d) makes
@@ -610,9 +602,15 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                                          common);
                     }
                 }
-                const uint32_t any = finish_scan<S>(wmask, lane, common, alive);
+                finish_scan<S>(wmask, lane, common, alive);
                 ++bscans;
-                if (!__any_sync(kFull, any != 0u)) {  // skip rule for the whole block
+                {  // one warp reduction gives the skip rule and the hand-off test
+                    int na = 0;
+#pragma unroll
+                    for (int k = 0; k < B::KW; ++k) na += __popc(alive[k]);
+                    nalive = __reduce_add_sync(kFull, na);
+                }
+                if (nalive == 0) {  // skip rule for the whole block
                     dead = true;
                     if (a.skip) break;  // (a.skip == 0: plain brute force scans on)
                 }
