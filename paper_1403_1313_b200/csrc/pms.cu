@@ -209,8 +209,8 @@ const uint32_t* ensure_ball_table(int dev) {
     std::lock_guard<std::mutex> lk(g_ball_mu);
     if (dev < 0 || dev >= 64) return nullptr;
     if (!g_ball[dev]) {
-        std::vector<uint32_t> h(kTWords);
-        for (int idx = 0; idx < kTWords; ++idx) {
+        std::vector<uint32_t> h(kTWords, 0u);
+        for (int idx = 0; idx < kR1Off; ++idx) {
             const uint32_t m = idx & 31u, e = (idx >> 5) & 31u;
             const int rho = idx >> 10;
             uint32_t w = 0;
@@ -218,6 +218,9 @@ const uint32_t* ensure_ball_table(int dev) {
                 if (__builtin_popcount(m | (b ^ e)) <= rho) w |= 1u << b;
             h[idx] = w;
         }
+        static const int kM[6] = {0, 1, 2, 4, 8, 16};  // radius-1 rows, packed (see kR1Off)
+        for (int e = 0; e < 32; ++e)
+            for (int j = 0; j < 6; ++j) h[kR1Off + e * 8 + j] = h[1024 + e * 32 + kM[j]];
         uint32_t* d = nullptr;
         if (cudaMalloc(&d, kTWords * 4) != cudaSuccess) return nullptr;
         if (cudaMemcpy(d, h.data(), kTWords * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -354,7 +357,7 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         static_smem = (uint32_t)fb.sharedSizeBytes;
     }
     const uint32_t ball_bytes =
-        block_algo ? (uint32_t)kTWords * 4u : 0u;  // ball table (28 KB)
+        block_algo ? (uint32_t)kTWords * 4u : 0u;  // ball table (29 KB)
     // block family with a register tile: per-warp hit queue (u16 window
     // indices, 32*NW per warp, sized for the largest CTA)
     const uint32_t queue_bytes =

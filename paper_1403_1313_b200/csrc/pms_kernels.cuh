@@ -318,7 +318,11 @@ struct BlkTraits {
     static constexpr uint32_t M = (1u << S) - 1u;        // suffix plane mask
 };
 constexpr int kTRows = 7;                                // rho = 0..6 (5, 6: all ones)
-constexpr int kTWords = kTRows * 1024;                   // 28 KB ball table
+// + 32 x 8 words: the six radius-1 words resolve_hit needs per e = eL & 31,
+// T[1][e][m] for m = 0, 1, 2, 4, 8, 16 (two pad words), packed for two 16-B
+// loads (the rows of T itself would put every lane's T[1][e][0] in one bank)
+constexpr int kR1Off = kTRows * 1024;
+constexpr int kTWords = kR1Off + 32 * 8;                 // 29 KB ball table
 
 // Suffix code (S digits, big-endian base 4) of the block candidate at
 // (lane, word k, bit b).
@@ -373,10 +377,12 @@ __device__ __forceinline__ uint32_t resolve_hit(typename P::word w, uint2 cb, ui
         return kFull;
     }
     if (p + 1u == dp) {
-        const uint32_t* T1 = T + 1024 + (el5 << 5);
-        atomicOr(wmask + widx<S>(eh5, ek), T1[0]);
+        const uint4* R = reinterpret_cast<const uint4*>(T + kR1Off + (el5 << 3));
+        const uint4 r0 = R[0], r1 = R[1];
+        const uint32_t t1[6] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y};  // m = 0, 1, 2, 4, 8, 16
+        atomicOr(wmask + widx<S>(eh5, ek), t1[0]);
 #pragma unroll
-        for (int q = 0; q < 5; ++q) atomicOr(wmask + widx<S>(eh5 ^ (1u << q), ek), T1[1u << q]);
+        for (int q = 0; q < 5; ++q) atomicOr(wmask + widx<S>(eh5 ^ (1u << q), ek), t1[q + 1]);
 #pragma unroll
         for (int u = 0; u < 3 * B::X; ++u)
             atomicOr(wmask + widx<S>(eh5, ek ^ up1_delta(B::X, u)), 1u << el5);
