@@ -130,13 +130,18 @@ __global__ void __launch_bounds__(kBlock) pms_search_reg(SearchArgs a) {
 // ------------------------------------------------ block-family instances
 #define PMS_BLK5(nw) {5, nw, pms_search_block<Bp32, 5, true, nw>, pms_search_block<Bp32, 5, false, nw>},
 #define PMS_BLK6(nw) {6, nw, pms_search_block<Bp32, 6, true, nw>, pms_search_block<Bp32, 6, false, nw>},
+// Block-family register tiles stop at 32 windows per lane (the per-lane hit
+// mask is one 32-bit word); longer rows stream through the NW = 0 kernel.
+#define PMS_NWB_LIST(X) \
+    X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10) X(12) X(14) X(16) X(19) X(22) X(25) X(28) \
+    X(31) X(32)
 // per S: the generic (NW = 0) instance first, then register tiles ascending
 // (S = 7 -- 16 words per lane -- was measured slower: (15,4) 0.46-0.52 ms vs
 // 0.378, (16,5) 8.7-10.2 ms vs 4.8; its scans cost 4.7x an S = 6 scan)
 const BlockKernel kBlockKernels[] = {
     {5, 0, pms_search_block<Bp32, 5, true, 0>, pms_search_block<Bp32, 5, false, 0>},
     {6, 0, pms_search_block<Bp32, 6, true, 0>, pms_search_block<Bp32, 6, false, 0>},
-    PMS_NW_LIST(PMS_BLK5) PMS_NW_LIST(PMS_BLK6)};
+    PMS_NWB_LIST(PMS_BLK5) PMS_NWB_LIST(PMS_BLK6)};
 
 // ---------------------------------------------------- roofline microbenchmark
 // The exact per-compare sequence of pms_search_reg<G,NW> (same register-

@@ -508,6 +508,7 @@ template <class P, int S, bool SMEM, int NW>
 __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(SearchArgs a) {
     using B = BlkTraits<S>;
     using word = typename P::word;
+    static_assert(NW <= 32, "the per-lane hit mask holds 32 windows");
     extern __shared__ __align__(128) uint32_t stab[];  // [ball table T][window table if SMEM]
     __shared__ __align__(8) uint64_t bar;
     __shared__ __align__(16) uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp r = 0 hits

@@ -543,3 +543,21 @@ def test_graph_replay_sees_new_inputs(orc):
     assert pms.find_ex(bad, 9, 2, lo=1000, hi=90000, want_stats=False).status == pms.E_CHAR
     assert pms.find_ex(b, 9, 2, lo=1000, hi=90000, want_stats=False).codes.tolist() == \
         orc.find(b, 9, 2, lo=1000, hi=90000).codes.tolist()
+
+
+@pytest.mark.parametrize("W", [992, 1024, 1025, 1100, 1300, 1536, 1537, 1600])
+def test_block_algo_long_rows(orc, W):
+    """Rows of 1025..1536 windows (regression: the block family once used
+    register tiles of more than 32 windows per lane there, overflowing the
+    per-lane 32-bit hit mask); both block sizes, the hand-off, a global table,
+    and the 64-bit words."""
+    l, d = 8, 1
+    s, _ = fmgen.generate_fm(3, W + l - 1, l, d, W)
+    for L in [pms.Launch(), pms.Launch(algo=pms.ALGO_BLOCK, block_digits=5),
+              pms.Launch(algo=pms.ALGO_BLOCK, block_digits=6, handoff=17),
+              pms.Launch(algo=pms.ALGO_BLOCK, table_global=1),
+              pms.Launch(algo=pms.ALGO_BLOCK, wide_words=1)]:
+        assert_same(s, l, d, orc, launch=L)
+    s2 = fmgen.random_sequences(12, W + 13, W + 1)  # l = 14, dense hits, ranges
+    for lo in (0, 4 ** 14 // 3):
+        assert_same(s2, 14, 4, orc, lo=lo, hi=lo + 20000)
