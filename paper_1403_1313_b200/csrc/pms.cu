@@ -71,7 +71,7 @@ template <int G, int NW, bool SMEM>
 __global__ void __launch_bounds__(kBlock) pms_search_reg(SearchArgs a) {
     extern __shared__ __align__(128) uint32_t stab[];
     __shared__ __align__(8) uint64_t bar;
-    if (*(volatile unsigned int*)&a.st->bad) return;  // invalid input: no work
+    if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;  // invalid input: no work
     if (SMEM) stage_table(a, stab, &bar);
     const uint32_t* tab = SMEM ? stab : static_cast<const uint32_t*>(a.tab);
 
@@ -262,6 +262,7 @@ struct pms_plan {
     const uint32_t* d_ball = nullptr;  // the device's ball table (block family; not owned)
     DevState* d_state = nullptr;
     DevState* h_state = nullptr;  // pinned mirror, read back by pms_plan_wait
+    uint32_t epoch = 0;           // id of the last step (h_state->bad == epoch: invalid input)
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // start, packed, searched
     cudaStream_t aux = nullptr;   // private stream for the state read-back
     SearchFn fn = nullptr;
@@ -437,7 +438,8 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     if (p->launch.grid_ctas > 0) p->grid = std::min((int)p->launch.grid_ctas, p->grid);
     if (cudaMalloc(&p->d_table, p->tab_bytes) != cudaSuccess ||
         cudaMalloc(&p->d_state, sizeof(DevState)) != cudaSuccess ||
-        cudaMallocHost(&p->h_state, sizeof(DevState)) != cudaSuccess) {
+        cudaMallocHost(&p->h_state, sizeof(DevState)) != cudaSuccess ||
+        cudaMemset(p->d_state, 0, sizeof(DevState)) != cudaSuccess) {
         destroy_plan(p);
         return fail_cuda(__LINE__);
     }
@@ -498,16 +500,17 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     a.st = p->d_state; a.nout = reinterpret_cast<unsigned long long*>(d_count);
     a.out = d_out; a.out_wide = out_wide; a.cap = cap;
     a.ball = p->d_ball;
+    if (++p->epoch == 0) p->epoch = 1;  // 0 is the reset value of st->bad
+    a.epoch = p->epoch;
 
-    // device work of a step: state reset, pre-pass (which also zeroes the
+    // device work of a step: pre-pass (which also resets the state and the
     // result counter), search; the state read-back is pms_plan_wait's
     if (cudaEventRecord(p->ev[0], s) != cudaSuccess) return fail_cuda(__LINE__);
-    if (cudaMemsetAsync(p->d_state, 0, sizeof(DevState), s) != cudaSuccess)
-        return fail_cuda(__LINE__);
-    const long long cells = (long long)p->n * p->Wp;
-    p->pack<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(d_seqs, p->n, p->t, p->l, p->W, p->Wp,
+    const long long pack_ctas = (long long)p->n * ((p->Wp + kPackThreads - 1) / kPackThreads);
+    p->pack<<<(unsigned)pack_ctas, kPackThreads, 0, s>>>(d_seqs, p->n, p->t, p->l, p->W, p->Wp,
                                                              p->d_table, p->d_state,
-                                                             reinterpret_cast<unsigned long long*>(d_count));
+                                                             reinterpret_cast<unsigned long long*>(d_count),
+                                                             p->epoch);
     const cudaError_t e_pack = cudaGetLastError();
     if (e_pack != cudaSuccess) return fail_cuda(__LINE__, e_pack);
     if (cudaEventRecord(p->ev[1], s) != cudaSuccess) return fail_cuda(__LINE__);
@@ -552,7 +555,7 @@ void fill_stats(pms_plan* p, pms_stats* stats) {
     // compares per (block, sequence) scan + W per per-candidate scan.
     const bool seq0_implicit = !p->generic && p->algo == PMS_ALGO_CANDIDATE;
     stats->issued_compares =
-        p->h_state->bad ? 0
+        p->h_state->bad == p->epoch ? 0
                         : (seq0_implicit ? cands * W : 0) +
                               (p->h_state->extra + p->h_state->block_scans) * W;
     stats->algo = p->algo;
@@ -579,7 +582,7 @@ extern "C" int pms_plan_wait(pms_plan* p, pms_stats* stats) {
         cudaStreamSynchronize(p->aux) != cudaSuccess)
         return fail_cuda(__LINE__);
     if (stats) fill_stats(p, stats);
-    return p->h_state->bad ? PMS_E_CHAR : PMS_OK;
+    return p->h_state->bad == p->epoch ? PMS_E_CHAR : PMS_OK;
 }
 
 // ========================================================================
@@ -610,6 +613,7 @@ struct CallCtx {
     unsigned long long g_lo = 0, g_hi = 0, g_cap = 0;
     int g_wide = -1, g_disabled = 0;
     void* g_out = nullptr;
+    uint32_t g_epoch = 0;  // the plan step id baked into the graph's pre-pass
     // previous call's parameters: a graph is captured only for a repeat
     unsigned long long p_lo = ~0ull, p_hi = 0, p_cap = 0;
     int p_wide = -1;
@@ -778,6 +782,7 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
                     cudaGraphInstantiate(&c->gexec, g, 0) == cudaSuccess) {
                     c->g_lo = lo; c->g_hi = hi; c->g_cap = cap; c->g_wide = kWide;
                     c->g_out = c->d_out;
+                    c->g_epoch = pl->epoch;
                 } else {
                     c->gexec = nullptr;
                     c->g_disabled = 1;
@@ -794,6 +799,7 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
                 return fail_cuda(__LINE__);
             }
             graphed = true;
+            pl->epoch = c->g_epoch;  // the step id the graph's pre-pass stores on bad input
         }
     }
     if (!graphed) {
@@ -808,7 +814,15 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
         return fail_cuda(__LINE__);
     }
     if (stats) fill_stats(pl, stats);
-    if (pl->h_state->bad) return PMS_E_CHAR;
+    if (pl->h_state->bad == pl->epoch) {
+        // a replayed graph reuses its step id: clear the flag for the next call
+        if (cudaMemsetAsync(&pl->d_state->bad, 0, sizeof(unsigned int), s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            healthy = false;
+            return fail_cuda(__LINE__);
+        }
+        return PMS_E_CHAR;
+    }
     const uint64_t found = *c->h_count;
     if (stats) stats->motifs = found;
     *count = found;

@@ -38,7 +38,7 @@ struct DevState {
     unsigned long long next;    // work counter: candidates handed out, from lo_al
     unsigned long long extra;   // sequences scanned beyond sequence 0 (survivors)
     unsigned long long block_scans;  // PMS_ALGO_BLOCK (block, sequence) scans
-    unsigned int bad;           // pre-pass saw a byte outside ACGTacgt
+    unsigned int bad;           // = the step's epoch: its pre-pass saw a byte outside ACGTacgt
     unsigned int pad[3];
 };
 

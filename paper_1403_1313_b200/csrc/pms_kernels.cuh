@@ -38,6 +38,7 @@ struct SearchArgs {
     uint32_t tab_bytes;
     const uint32_t* ball;           // the ball table T in global memory (built once per device)
     DevState* st;
+    uint32_t epoch;                 // this step's id; st->bad == epoch: invalid input
     unsigned long long* nout;       // result counter (caller's d_count)
     void* out;                      // result buffer, capacity cap (uint32 or uint64)
     unsigned long long cap;
@@ -45,7 +46,7 @@ struct SearchArgs {
 
 using SearchFn = void (*)(SearchArgs);
 using PackFn = void (*)(const uint8_t*, int, int, int, int, int, void*, DevState*,
-                        unsigned long long*);
+                        unsigned long long*, uint32_t);
 
 struct BlockKernel {
     int S, NW;
@@ -157,31 +158,54 @@ using namespace pms;
 // One thread per (sequence i, window k < Wp).  Window k (the length-l
 // substring starting at k, k in [0, W)) is packed into a bit-plane word; rows
 // are padded to Wp with copies of window W-1, which cannot change "some window
-// is within d".  Every byte lies in at least one window, so the byte check
-// covers the whole input.
-// Thread 0 also zeroes the caller's result counter (saves a memset launch).
+// is within d".  A CTA takes kPackThreads consecutive windows of one row: its
+// bytes are staged (one independent load each, so a cold input costs one HBM
+// latency instead of l dependent ones) and checked once per byte; every byte
+// lies in at least one window, so the byte check covers the whole input.
+// Thread 0 also resets the step's state and the caller's result counter (no
+// memset launch); an invalid byte stores the step's epoch in st->bad, so a
+// stale flag of an earlier step never needs clearing.
+constexpr int kPackThreads = 256;
 template <class P>
-__global__ void pms_pack_kernel(const uint8_t* __restrict__ seqs, int n, int t, int l, int W,
-                                int Wp, void* __restrict__ tab_, DevState* st,
-                                unsigned long long* nout) {
+__global__ void __launch_bounds__(kPackThreads) pms_pack_kernel(
+    const uint8_t* __restrict__ seqs, int n, int t, int l, int W, int Wp, void* __restrict__ tab_,
+    DevState* st, unsigned long long* nout, uint32_t epoch) {
+    __shared__ uint8_t code[kPackThreads + 32];  // 2-bit codes of the CTA's bytes, 4 = invalid
     typename P::word* tab = static_cast<typename P::word*>(tab_);
-    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (idx == 0) *nout = 0ull;
-    if (idx >= (long long)n * Wp) return;
-    const int i = (int)(idx / Wp);
-    const int k = (int)(idx - (long long)i * Wp);
-    const uint8_t* p = seqs + (long long)i * t + min(k, W - 1);
-    uint32_t H = 0, L = 0, bad = 0;
-    PMS_CHECK(min(k, W - 1) + l <= t);
-    for (int j = 0; j < l; ++j) {
-        const uint32_t u = p[j] & 0xDFu;  // upper-case; only 'x'/'X' map to 'X'
-        const uint32_t code = u == 'A' ? 0u : u == 'C' ? 1u : u == 'G' ? 2u : u == 'T' ? 3u : 4u;
-        bad |= code >> 2;
-        H = (H << 1) | ((code >> 1) & 1u);
-        L = (L << 1) | (code & 1u);
+    const int chunks = (Wp + kPackThreads - 1) / kPackThreads;
+    const int i = (int)(blockIdx.x / (unsigned)chunks);
+    const int k0 = (int)(blockIdx.x - (unsigned)i * chunks) * kPackThreads;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *nout = 0ull;
+        st->next = 0ull;
+        st->extra = 0ull;
+        st->block_scans = 0ull;
     }
-    tab[idx] = P::pack(H, L, l);
-    if (bad) atomicOr(&st->bad, 1u);
+    if (i >= n) return;
+    // bytes [s0, s1) of row i feed windows k0 .. k0 + kPackThreads - 1 (clamped to W-1)
+    const int s0 = min(k0, W - 1);
+    const int s1 = min(k0 + kPackThreads - 1, W - 1) + l;
+    PMS_CHECK(s1 <= t && s1 - s0 <= kPackThreads + 32);
+    const uint8_t* row = seqs + (long long)i * t;
+    uint32_t bad = 0;
+    for (int b = s0 + (int)threadIdx.x; b < s1; b += kPackThreads) {
+        const uint32_t u = row[b] & 0xDFu;  // upper-case; only 'x'/'X' map to 'X'
+        const uint32_t c = u == 'A' ? 0u : u == 'C' ? 1u : u == 'G' ? 2u : u == 'T' ? 3u : 4u;
+        bad |= c >> 2;
+        code[b - s0] = (uint8_t)c;
+    }
+    if (bad) *(volatile unsigned int*)&st->bad = epoch;
+    __syncthreads();
+    const int k = k0 + (int)threadIdx.x;
+    if (k >= Wp) return;
+    const uint8_t* q = code + (min(k, W - 1) - s0);
+    uint32_t H = 0, L = 0;
+    for (int j = 0; j < l; ++j) {
+        const uint32_t c = q[j];
+        H = (H << 1) | ((c >> 1) & 1u);
+        L = (L << 1) | (c & 1u);
+    }
+    tab[(long long)i * Wp + k] = P::pack(H, L, l);
 }
 
 // ------------------------------------------------------------- shared pieces
@@ -248,7 +272,7 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
     using word = typename P::word;
     extern __shared__ __align__(128) unsigned char gsm[];
     __shared__ __align__(8) uint64_t bar;
-    if (*(volatile unsigned int*)&a.st->bad) return;
+    if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
     if (SMEM) stage_table(a, gsm, &bar);
     const word* tab = SMEM ? reinterpret_cast<const word*>(gsm) : static_cast<const word*>(a.tab);
     const int lane = threadIdx.x & 31;
@@ -512,7 +536,7 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
     extern __shared__ __align__(128) uint32_t stab[];  // [ball table T][window table if SMEM]
     __shared__ __align__(8) uint64_t bar;
     __shared__ __align__(16) uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp r = 0 hits
-    if (*(volatile unsigned int*)&a.st->bad) return;
+    if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
     uint32_t* T = stab;
     uint32_t* wmask = wmasks[threadIdx.x >> 5];
 #pragma unroll
