@@ -137,6 +137,10 @@ typedef struct pms_stats {
  * A call without stats that repeats the previous call's shape, range and
  * capacity (same pooled context) replays the device work as one CUDA graph;
  * set the environment variable PMS_NO_GRAPH to always enqueue it call by call.
+ * The search kernel is a programmatic dependent launch of the pre-pass (it
+ * waits in-kernel for the pre-pass's writes); without stats no timing event
+ * separates the two, so its launch overlaps the pre-pass (PMS_NO_PDL: plain
+ * stream order).
  * ------------------------------------------------------------------- */
 int pms_find(const uint8_t *seqs, int32_t n, int32_t t, int32_t l, int32_t d,
              uint32_t *out_codes, uint64_t max_out, uint64_t *count);

@@ -71,6 +71,7 @@ template <int G, int NW, bool SMEM>
 __global__ void __launch_bounds__(kBlock) pms_search_reg(SearchArgs a) {
     extern __shared__ __align__(128) uint32_t stab[];
     __shared__ __align__(8) uint64_t bar;
+    pdl_wait();
     if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;  // invalid input: no work
     if (SMEM) stage_table(a, stab, &bar);
     const uint32_t* tab = SMEM ? stab : static_cast<const uint32_t*>(a.tab);
@@ -461,8 +462,10 @@ extern "C" void pms_plan_destroy(pms_plan* plan) { destroy_plan(plan); }
 namespace {
 
 // out_wide: d_out holds uint64 codes (pms_plan_execute64) instead of uint32
+// timed = false (pms_find* without stats): no event between the pre-pass and
+// the search kernel, so the programmatic dependent launch overlaps them.
 int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, void* d_out,
-                 int out_wide, uint64_t cap, uint64_t* d_count, void* stream) {
+                 int out_wide, uint64_t cap, uint64_t* d_count, void* stream, bool timed = true) {
     if (!p || !d_seqs || !d_count || (!d_out && cap > 0)) return PMS_E_ARG;
     if (!out_wide && p->l > PMS_MAX_L) return PMS_E_ARG;  // codes would not fit uint32
     const unsigned long long total = 1ull << (2 * p->l);
@@ -513,10 +516,21 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
                                                              p->epoch);
     const cudaError_t e_pack = cudaGetLastError();
     if (e_pack != cudaSuccess) return fail_cuda(__LINE__, e_pack);
-    if (cudaEventRecord(p->ev[1], s) != cudaSuccess) return fail_cuda(__LINE__);
+    if (timed && cudaEventRecord(p->ev[1], s) != cudaSuccess) return fail_cuda(__LINE__);
     if (span > 0) {
-        p->fn<<<p->grid, p->block, p->smem_bytes, s>>>(a);
-        const cudaError_t e = cudaGetLastError();
+        // programmatic dependent launch after the pre-pass (PMS_NO_PDL: plain)
+        static const bool no_pdl = std::getenv("PMS_NO_PDL") != nullptr;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)p->grid);
+        cfg.blockDim = dim3((unsigned)p->block);
+        cfg.dynamicSmemBytes = (size_t)p->smem_bytes;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = no_pdl ? 0 : 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, p->fn, a);
         if (e != cudaSuccess) return fail_cuda(__LINE__, e);
     }
     if (cudaEventRecord(p->ev[2], s) != cudaSuccess) return fail_cuda(__LINE__);
@@ -749,7 +763,8 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
         if (cudaMemcpyAsync(c->d_seqs, c->h_seqs, (size_t)n * t, cudaMemcpyHostToDevice, s) !=
             cudaSuccess)
             return fail_cuda(__LINE__);
-        const int e = plan_execute(pl, c->d_seqs, lo, hi, c->d_out, kWide, cap, c->d_count, s);
+        const int e = plan_execute(pl, c->d_seqs, lo, hi, c->d_out, kWide, cap, c->d_count, s,
+                                   stats != nullptr);
         if (e != PMS_OK) return e;
         if (cudaMemcpyAsync(pl->h_state, pl->d_state, sizeof(DevState), cudaMemcpyDeviceToHost,
                             s) != cudaSuccess ||

@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(kPackThreads) pms_pack_kernel(
     const uint8_t* __restrict__ seqs, int n, int t, int l, int W, int Wp, void* __restrict__ tab_,
     DevState* st, unsigned long long* nout, uint32_t epoch) {
     __shared__ uint8_t code[kPackThreads + 32];  // 2-bit codes of the CTA's bytes, 4 = invalid
+    pdl_launch_dependents();
     typename P::word* tab = static_cast<typename P::word*>(tab_);
     const int chunks = (Wp + kPackThreads - 1) / kPackThreads;
     const int i = (int)(blockIdx.x / (unsigned)chunks);
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kBlock) pms_search_generic(SearchArgs a) {
     using word = typename P::word;
     extern __shared__ __align__(128) unsigned char gsm[];
     __shared__ __align__(8) uint64_t bar;
+    pdl_wait();
     if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
     if (SMEM) stage_table(a, gsm, &bar);
     const word* tab = SMEM ? reinterpret_cast<const word*>(gsm) : static_cast<const word*>(a.tab);
@@ -536,6 +538,7 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
     extern __shared__ __align__(128) uint32_t stab[];  // [ball table T][window table if SMEM]
     __shared__ __align__(8) uint64_t bar;
     __shared__ __align__(16) uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp r = 0 hits
+    pdl_wait();
     if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
     uint32_t* T = stab;
     uint32_t* wmask = wmasks[threadIdx.x >> 5];
