@@ -502,25 +502,45 @@ __device__ __forceinline__ void drain_hits(uint32_t hm, int top, const typename 
 // lanes' hit counts, then each lane writes its own), and the queue is
 // processed 32 hits per round -- typically one or two rounds, where the
 // per-lane drain needs max-over-lanes(hits) rounds of the same work.
+// Queue slots by a shared-memory atomic per lane (1) or a warp prefix sum
+// (0); default (-1): atomic for 32-bit words (measured -0.6 % at (15,4),
+// -0.7 % at (16,5)), prefix sum for 64-bit words (atomic: +5..7 % at (17,6),
+// (19,7), whose scans carry many more hits).
+#ifndef PMS_QUEUE_ATOMIC
+#define PMS_QUEUE_ATOMIC -1
+#endif
 template <class P, int S>
 __device__ __forceinline__ void drain_queue(uint32_t hm, int top, const typename P::word* row,
-                                            uint16_t* queue, uint2 cb, uint32_t dp, int lane,
-                                            const uint32_t* T, uint32_t* wmask, uint32_t& common) {
+                                            uint16_t* queue, uint32_t* qcnt, uint2 cb, uint32_t dp,
+                                            int lane, const uint32_t* T, uint32_t* wmask,
+                                            uint32_t& common) {
+    constexpr bool kAtomic =
+        PMS_QUEUE_ATOMIC > 0 || (PMS_QUEUE_ATOMIC < 0 && sizeof(typename P::word) == 4);
     const uint32_t nh = __popc(hm);
-    uint32_t inc = nh;  // inclusive prefix sum of the hit counts over lanes
+    uint32_t pos, total;
+    if (kAtomic) {
+        // lanes claim their queue slots with one shared-memory atomic each
+        // (any order of the lanes is a valid queue); the warp's counter is
+        // reset once the slots are claimed
+        pos = atomicAdd(qcnt, nh);
+        total = __reduce_add_sync(kFull, nh);
+    } else {
+        uint32_t inc = nh;  // inclusive prefix sum of the hit counts over lanes
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(kFull, inc, o);
-        if (lane >= o) inc += v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += v;
+        }
+        total = __shfl_sync(kFull, inc, 31);
+        pos = inc - nh;
     }
-    const uint32_t total = __shfl_sync(kFull, inc, 31);
-    uint32_t pos = inc - nh;
     while (hm) {
         const int q = msb(hm);
         hm &= ~(1u << q);
         queue[pos++] = (uint16_t)(lane + 32 * (top - q));
     }
     __syncwarp();
+    if (kAtomic && lane == 0) *qcnt = 0u;  // next use is after finish_scan's __syncwarp
     for (uint32_t base = 0; base < total; base += 32) {
         uint32_t mine = kFull;
         if (base + lane < total) mine = resolve_hit<P, S>(row[queue[base + lane]], cb, dp, T, wmask);
@@ -538,12 +558,14 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
     extern __shared__ __align__(128) uint32_t stab[];  // [ball table T][window table if SMEM]
     __shared__ __align__(8) uint64_t bar;
     __shared__ __align__(16) uint32_t wmasks[kBlockB / 32][32 * B::KW];  // per-warp r = 0 hits
+    __shared__ uint32_t qcnts[kBlockB / 32];  // per-warp queue counters (atomic slots)
     pdl_wait();
     if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
     uint32_t* T = stab;
     uint32_t* wmask = wmasks[threadIdx.x >> 5];
 #pragma unroll
     for (int k = 0; k < B::KW; ++k) wmask[widx<S>(threadIdx.x & 31, k)] = 0u;
+    if ((threadIdx.x & 31) == 0) qcnts[threadIdx.x >> 5] = 0u;
     word* tsm = reinterpret_cast<word*>(stab + kTWords);  // 128-B aligned for the bulk copy
     // prologue: TMA bulk copies of the ball table (28 KB, precomputed once per
     // device) and, when staged, the window table into shared memory
@@ -620,7 +642,8 @@ __global__ void __launch_bounds__(kBlockB, PMS_BLK_MIN_CTAS) pms_search_block(Se
                     hm &= real;
                     // pass 2: resolve the hits into each lane's candidate words
                     if (PMS_QUEUE_DRAIN)
-                        drain_queue<P, S>(hm, NW - 1, row, queue, cb, a.dp, lane, T, wmask, common);
+                        drain_queue<P, S>(hm, NW - 1, row, queue, &qcnts[threadIdx.x >> 5], cb, a.dp,
+                                          lane, T, wmask, common);
                     else
                         drain_hits<P, S>(hm, NW - 1, row, a.Wp, cb, a.dp, lane, T, wmask, common);
                 } else {
