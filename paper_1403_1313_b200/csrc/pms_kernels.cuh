@@ -534,10 +534,11 @@ __device__ __forceinline__ void drain_queue(uint32_t hm, int top, const typename
         total = __shfl_sync(kFull, inc, 31);
         pos = inc - nh;
     }
+    const int qbase = lane + 32 * top;  // window of hit bit q: qbase - 32 q
     while (hm) {
         const int q = msb(hm);
-        hm &= ~(1u << q);
-        queue[pos++] = (uint16_t)(lane + 32 * (top - q));
+        hm ^= 1u << q;
+        queue[pos++] = (uint16_t)(qbase - 32 * q);
     }
     __syncwarp();
     if (kAtomic && lane == 0) *qcnt = 0u;  // next use is after finish_scan's __syncwarp
