@@ -430,10 +430,10 @@ def run_gpu(args) -> int:
         "cpu_baseline": cpu,
         "e2e": {"value": (1 if strong else world) * args.e2e_steps * total / (e2e_tot * 1e-3),
                 "unit": "candidates/s", "h2d_bytes_per_step": n * t,
-                # state (32 B) + count (8 B) + the first min(cap, 1024) codes copied
-                # with them (include/pms.h: one round trip for small sets), + the
-                # codes again when the set is larger than that
-                "d2h_bytes_per_step": 32 + 8 + 4 * min(cap, 1024) + (4 * nfound if nfound > 1024 else 0),
+                # one copy of the result block's 128-B head (state + count) and the
+                # first min(cap, 1024) codes (include/pms.h: one round trip for
+                # small sets), + the codes again when the set is larger than that
+                "d2h_bytes_per_step": 128 + 4 * min(cap, 1024) + (4 * nfound if nfound > 1024 else 0),
                 "path": "pms_find_ex from host buffers (pooled context, H2D, kernels, D2H, sort)"},
         "gpu_launches": 2 * args.steps,
         "clocks": cs,

@@ -132,8 +132,9 @@ typedef struct pms_stats {
  * An empty result is PMS_OK with *count = 0; d >= l yields all 4^l codes.
  * Steps: validate arguments -> H2D copy -> device pre-pass (byte check +
  * window packing) -> persistent search kernel with in-kernel atomic-append
- * compaction -> D2H of the state, the count and the first min(max_out, 1024)
- * codes in one round trip (the rest only if the set is larger) -> host sort.
+ * compaction -> one D2H copy of the state, the count and the first
+ * min(max_out, 1024) codes (contiguous in the context's result block; the
+ * rest only if the set is larger) -> host sort.
  * A call without stats that repeats the previous call's shape, range and
  * capacity (same pooled context) replays the device work as one CUDA graph;
  * set the environment variable PMS_NO_GRAPH to always enqueue it call by call.

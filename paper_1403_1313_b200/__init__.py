@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -73,13 +74,15 @@ def load() -> ctypes.CDLL:
         i32, u64 = ctypes.c_int32, ctypes.c_uint64
         lib.pms_find.argtypes = [u8p, i32, i32, i32, i32, u32p, u64, u64p]
         lib.pms_find.restype = ctypes.c_int
-        lib.pms_find_ex.argtypes = [u8p, i32, i32, i32, i32, u64, u64, ctypes.POINTER(Launch),
-                                    u32p, u64, u64p, ctypes.POINTER(Stats)]
+        # (void* for the byte and code buffers: _find_ex passes raw addresses,
+        # which skips a ctypes pointer object per call)
+        lib.pms_find_ex.argtypes = [vp, i32, i32, i32, i32, u64, u64, ctypes.POINTER(Launch),
+                                    vp, u64, u64p, ctypes.POINTER(Stats)]
         lib.pms_find_ex.restype = ctypes.c_int
         lib.pms_find64.argtypes = [u8p, i32, i32, i32, i32, u64p, u64, u64p]
         lib.pms_find64.restype = ctypes.c_int
-        lib.pms_find64_ex.argtypes = [u8p, i32, i32, i32, i32, u64, u64, ctypes.POINTER(Launch),
-                                      u64p, u64, u64p, ctypes.POINTER(Stats)]
+        lib.pms_find64_ex.argtypes = [vp, i32, i32, i32, i32, u64, u64, ctypes.POINTER(Launch),
+                                      vp, u64, u64p, ctypes.POINTER(Stats)]
         lib.pms_find64_ex.restype = ctypes.c_int
         lib.pms_plan_create.argtypes = [i32, i32, i32, i32, ctypes.POINTER(Launch),
                                         ctypes.POINTER(vp)]
@@ -143,15 +146,28 @@ def _find_ex(fname, ctype, seqs, l, d, lo, hi, launch, max_out, want_stats) -> F
     n, t = a.shape
     if hi is None:
         hi = (1 << 64) - 1
-    out = np.empty(max(int(max_out), 1), dtype=np.uint32 if ctype is ctypes.c_uint32 else np.uint64)
+    out = _scratch(max(int(max_out), 1), np.uint32 if ctype is ctypes.c_uint32 else np.uint64)
     cnt = ctypes.c_uint64(0)
     st = Stats() if want_stats else None
-    status = getattr(lib, fname)(a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), n, t, l, d,
-                                 int(lo), int(hi), ctypes.byref(launch) if launch else None,
-                                 out.ctypes.data_as(ctypes.POINTER(ctype)), int(max_out),
-                                 ctypes.byref(cnt), ctypes.byref(st) if st is not None else None)
+    status = getattr(lib, fname)(a.ctypes.data, n, t, l, d, int(lo), int(hi),
+                                 ctypes.byref(launch) if launch else None, out.ctypes.data,
+                                 int(max_out), ctypes.byref(cnt),
+                                 ctypes.byref(st) if st is not None else None)
     k = min(int(cnt.value), int(max_out)) if status in (OK, E_TRUNCATED) else 0
     return FindResult(status, out[:k].copy(), int(cnt.value), st)
+
+
+_tls = threading.local()
+
+
+def _scratch(size: int, dtype) -> np.ndarray:
+    """Per-thread code buffer reused across calls (results are copied out)."""
+    key = np.dtype(dtype).char
+    buf = getattr(_tls, key, None)
+    if buf is None or buf.size < size:
+        buf = np.empty(size, dtype=dtype)
+        setattr(_tls, key, buf)
+    return buf[:size]
 
 
 def find_ex(seqs, l: int, d: int, lo: int = 0, hi: int | None = None,

@@ -263,6 +263,7 @@ struct pms_plan {
     const uint32_t* d_ball = nullptr;  // the device's ball table (block family; not owned)
     DevState* d_state = nullptr;
     DevState* h_state = nullptr;  // pinned mirror, read back by pms_plan_wait
+    bool state_external = false;  // d_state lives in a pms_find context's result block
     uint32_t epoch = 0;           // id of the last step (h_state->bad == epoch: invalid input)
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // start, packed, searched
     cudaStream_t aux = nullptr;   // private stream for the state read-back
@@ -290,7 +291,7 @@ int check_shape(int32_t n, int32_t t, int32_t l, int32_t d, int32_t max_l) {
 void destroy_plan(pms_plan* p) {
     if (!p) return;
     cudaFree(p->d_table);
-    cudaFree(p->d_state);
+    if (!p->state_external) cudaFree(p->d_state);
     cudaFreeHost(p->h_state);
     for (cudaEvent_t e : p->ev)
         if (e) cudaEventDestroy(e);
@@ -613,10 +614,16 @@ struct CallCtx {
     pms_launch launch{};
     pms_plan* plan = nullptr;
     uint8_t* d_seqs = nullptr;
-    void* d_out = nullptr;            // result codes (uint32 or uint64)
+    // one device block [plan state | count | codes]: a single D2H brings back
+    // the state, the count and the first kSpecCodes codes
+    static constexpr size_t kHead = 128;
+    static constexpr unsigned long long kSpecCodes = 1024;  // codes copied back with the count
+    char* d_buf = nullptr;            // kHead + out_bytes
+    void* d_out = nullptr;            // result codes (uint32 or uint64) = d_buf + kHead
     unsigned long long out_bytes = 0;
-    uint64_t* d_count = nullptr;
-    uint64_t* h_count = nullptr;  // pinned
+    uint64_t* d_count = nullptr;      // = d_buf + 64
+    char* h_head = nullptr;           // pinned mirror of the block's first kHead + 8 kSpecCodes bytes
+    uint64_t* h_count = nullptr;      // = h_head + 64
     uint8_t* h_seqs = nullptr;    // pinned staging of the input (n*t bytes)
     void* h_out = nullptr;        // pinned staging of small result sets
     static constexpr unsigned long long kHostOutBytes = 1ull << 19;
@@ -641,9 +648,8 @@ struct CallCtx {
         if (gexec) cudaGraphExecDestroy(gexec);
         destroy_plan(plan);
         cudaFree(d_seqs);
-        cudaFree(d_out);
-        cudaFree(d_count);
-        cudaFreeHost(h_count);
+        cudaFree(d_buf);
+        cudaFreeHost(h_head);
         cudaFreeHost(h_seqs);
         cudaFreeHost(h_out);
         if (stream) cudaStreamDestroy(stream);
@@ -652,7 +658,27 @@ struct CallCtx {
 
 // codes copied back speculatively with the count (one host round trip when
 // the result set is small, as it is for planted-motif instances)
-constexpr unsigned long long kSpecCodes = 1024;
+constexpr unsigned long long kSpecCodes = CallCtx::kSpecCodes;
+
+// (Re)allocate the context's result block for `bytes` of codes; its head holds
+// the plan's state (zeroed: no stale invalid-input flag) and the count.
+int ctx_grow(CallCtx* c, unsigned long long bytes) {
+    cudaFree(c->d_buf);
+    c->d_buf = nullptr;
+    c->d_out = nullptr;
+    c->d_count = nullptr;
+    c->out_bytes = 0;
+    if (cudaMalloc(&c->d_buf, CallCtx::kHead + bytes) != cudaSuccess ||
+        cudaMemset(c->d_buf, 0, CallCtx::kHead) != cudaSuccess)
+        return fail_cuda(__LINE__);
+    c->d_out = c->d_buf + CallCtx::kHead;
+    c->d_count = reinterpret_cast<uint64_t*>(c->d_buf + 64);
+    c->out_bytes = bytes;
+    if (!c->plan->state_external) cudaFree(c->plan->d_state);
+    c->plan->d_state = reinterpret_cast<DevState*>(c->d_buf);
+    c->plan->state_external = true;
+    return PMS_OK;
+}
 static_assert(kSpecCodes * 8 <= (1ull << 19), "fits the pinned staging buffer");
 
 std::mutex g_pool_mu;
@@ -685,14 +711,20 @@ int ctx_acquire(int32_t n, int32_t t, int32_t l, int32_t d, const pms_launch& L,
         delete c;
         return st;
     }
+    static_assert(sizeof(DevState) <= 64, "state + count fit the result block's head");
     if (cudaMalloc(&c->d_seqs, (size_t)n * t) != cudaSuccess ||
-        cudaMalloc(&c->d_count, sizeof(uint64_t)) != cudaSuccess ||
-        cudaMallocHost(&c->h_count, sizeof(uint64_t)) != cudaSuccess ||
+        cudaMallocHost(&c->h_head, CallCtx::kHead + 8 * kSpecCodes) != cudaSuccess ||
         cudaMallocHost(&c->h_seqs, (size_t)n * t) != cudaSuccess ||
         cudaMallocHost(&c->h_out, CallCtx::kHostOutBytes) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
         ctx_destroy(c);
         return fail_cuda(__LINE__);
+    }
+    c->h_count = reinterpret_cast<uint64_t*>(c->h_head + 64);
+    st = ctx_grow(c, 8 * kSpecCodes);
+    if (st != PMS_OK) {
+        ctx_destroy(c);
+        return st;
     }
     *out = c;
     return PMS_OK;
@@ -742,15 +774,12 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
     } guard{c, &healthy};
 
     const unsigned long long cap = std::min<unsigned long long>(max_out, hi - lo);
-    if (cap * sizeof(Code) > c->out_bytes) {  // grow the result buffer (kept for the next call)
-        cudaFree(c->d_out);
-        c->d_out = nullptr;
-        c->out_bytes = 0;
-        if (cudaMalloc(&c->d_out, cap * sizeof(Code)) != cudaSuccess) {
+    if (cap * sizeof(Code) > c->out_bytes) {  // grow the result block (kept for the next call)
+        st = ctx_grow(c, cap * sizeof(Code));
+        if (st != PMS_OK) {
             healthy = false;
-            return fail_cuda(__LINE__);
+            return st;
         }
-        c->out_bytes = cap * sizeof(Code);
     }
     cudaStream_t s = c->stream;
     std::memcpy(c->h_seqs, seqs, (size_t)n * t);  // pinned staging: the H2D is a true async DMA
@@ -766,12 +795,8 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
         const int e = plan_execute(pl, c->d_seqs, lo, hi, c->d_out, kWide, cap, c->d_count, s,
                                    stats != nullptr);
         if (e != PMS_OK) return e;
-        if (cudaMemcpyAsync(pl->h_state, pl->d_state, sizeof(DevState), cudaMemcpyDeviceToHost,
-                            s) != cudaSuccess ||
-            cudaMemcpyAsync(c->h_count, c->d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
-                cudaSuccess ||
-            (spec > 0 && cudaMemcpyAsync(c->h_out, c->d_out, spec * sizeof(Code),
-                                         cudaMemcpyDeviceToHost, s) != cudaSuccess))
+        if (cudaMemcpyAsync(c->h_head, c->d_buf, CallCtx::kHead + spec * sizeof(Code),
+                            cudaMemcpyDeviceToHost, s) != cudaSuccess)
             return fail_cuda(__LINE__);
         return PMS_OK;
     };
@@ -828,6 +853,7 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
         healthy = false;
         return fail_cuda(__LINE__);
     }
+    std::memcpy(pl->h_state, c->h_head, sizeof(DevState));
     if (stats) fill_stats(pl, stats);
     if (pl->h_state->bad == pl->epoch) {
         // a replayed graph reuses its step id: clear the flag for the next call
@@ -854,7 +880,7 @@ int find_host(const uint8_t* seqs, int32_t n, int32_t t, int32_t l, int32_t d, u
             }
             if (staged) std::memcpy(out_codes, c->h_out, found * sizeof(Code));
         } else {
-            std::memcpy(out_codes, c->h_out, found * sizeof(Code));
+            std::memcpy(out_codes, c->h_head + CallCtx::kHead, found * sizeof(Code));
         }
         std::sort(out_codes, out_codes + found);
     }

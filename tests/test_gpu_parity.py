@@ -134,6 +134,25 @@ def test_lowercase_and_invalid_bytes(orc):
     assert gpu(bad, 6, 1).status == pms.E_CHAR
 
 
+@pytest.mark.parametrize("l", [7, 16, 23])
+def test_invalid_byte_in_every_prepass_tile(l):
+    """The pre-pass checks each byte once, in the 256-window tile of its row
+    that stages it (tiles overlap by l-1 bytes): an invalid byte at a tile
+    edge, in the overlap, in the last window's tail or in the last row must
+    still be reported, in both word widths; the clean input searches normally."""
+    n, t = 3, 256 * 3 + l + 5
+    s = fmgen.random_sequences(n, t, 40 + l)
+    find = pms.find_ex if l <= 16 else pms.find64_ex
+    assert find(s, l, 1, lo=0, hi=5000, want_stats=False).status == 0
+    for i, j in [(0, 0), (1, 255), (1, 256), (0, 255 + l - 1), (2, 511 + l - 1), (2, 512),
+                 (2, t - 1), (0, t - l)]:
+        bad = s.copy()
+        bad[i, j] = ord("N")
+        r = find(bad, l, 1, lo=0, hi=5000, want_stats=False)
+        assert r.status == pms.E_CHAR and r.count == 0, (i, j)
+        assert find(s, l, 1, lo=0, hi=5000, want_stats=False).status == 0
+
+
 def test_truncation_and_size_query(orc):
     s = fmgen.random_sequences(1, 12, 3)
     full = gpu(s, 5, 2)
