@@ -137,7 +137,9 @@ def run_reference(args) -> int:
     oracle.build()
     l, d = WORKLOAD["l"], WORKLOAD["d"]
     seqs, _ = fmgen.generate_fm(WORKLOAD["n"], WORKLOAD["t"], l, d, args.seed)
-    lo, n, cores = oracle_sample(l, d, seqs, args.ref_seconds)
+    # each step a bounded sample: the whole warm-up + timed run takes about
+    # --ref-seconds of CPU time whatever --steps is (minimum 2^14 codes a step)
+    lo, n, cores = oracle_sample(l, d, seqs, args.ref_seconds / max(1, args.steps + args.warmup))
     times, work = [], 0
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -458,7 +460,7 @@ def main() -> int:
     ap.add_argument("--rmix-steps", type=int, default=3,
                     help="steps of the block kernel without early exit (block-family R_mix)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-seconds", type=float, default=5.0)
+    ap.add_argument("--ref-seconds", type=float, default=60.0)  # whole --impl reference run
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
