@@ -16,7 +16,6 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1403_1313_b200 as pms  # noqa: E402
-sys.path.insert(0, os.path.join(ROOT, "inputs"))
 import fmgen  # noqa: E402
 
 

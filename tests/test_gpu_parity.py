@@ -591,3 +591,29 @@ def test_block_algo_long_rows(orc, W):
     s2 = fmgen.random_sequences(12, W + 13, W + 1)  # l = 14, dense hits, ranges
     for lo in (0, 4 ** 14 // 3):
         assert_same(s2, 14, 4, orc, lo=lo, hi=lo + 20000)
+
+
+@pytest.mark.parametrize("env", [{"PMS_NO_PDL": "1"}, {"PMS_NO_GRAPH": "1"},
+                                 {"PMS_NO_PDL": "1", "PMS_NO_GRAPH": "1"}])
+def test_plain_launch_paths(env):
+    """The switches read once per process (include/pms.h): plain stream order
+    instead of the programmatic dependent launch, and call-by-call enqueue
+    instead of graph replay, give the golden set of a BASELINE config, on
+    repeated calls (a fresh process per switch)."""
+    import subprocess
+    import sys
+    path = os.path.join(GOLDEN, "bj2_seed1.json")
+    code = f"""
+import json, sys
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import fmgen, paper_1403_1313_b200 as pms
+g = json.load(open({path!r}))
+s, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
+for _ in range(3):
+    r = pms.find_ex(s, g["l"], g["d"], want_stats=False)
+    assert r.status == 0 and r.codes.tolist() == g["codes"], r.status
+print("ok")
+"""
+    p = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stderr[-2000:]
