@@ -434,7 +434,7 @@ __device__ __forceinline__ void apply_broadcasts(uint32_t mine, int lane, const 
         who &= ~(1u << src);
         const uint32_t v = __shfl_sync(kFull, mine, src);
         const uint32_t off = (v ^ lane4) & 0xFFFFu;
-        PMS_CHECK(off < 4u * kTWords && off >= 4096u * B::X);
+        PMS_CHECK(off < 4u * kTWords && off + 1u > 4096u * B::X);
         const uint32_t a = *reinterpret_cast<const uint32_t*>(Tb + off);
         const uint32_t ek = v >> 16;
         atomicOr(wmask + widx<S>(lane, ek), a);  // the lane's own word: conflict-free
