@@ -1,8 +1,9 @@
 """CPU oracle for Skip-Brute-Force planted (l,d) motif search.
 
-TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
-``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
-package.  The product (``paper_1403_1313_b200``) never imports it, and this
+TEST INFRASTRUCTURE ONLY.  Only ``tests/`` (including the hand-run tools in
+``tests/tools/``), ``__graft_entry__.smoke()``, ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs and ``scripts/make_golden.py``
+(which writes the stored golden sets) may import this package.  The product (``paper_1403_1313_b200``) never imports it, and this
 package imports nothing from the product.
 
 The arithmetic lives in ``pms_oracle.c`` (plain C, character compares, see

@@ -1,6 +1,6 @@
 """Paper-experiment analogues on B200.  Run on the GPU box:
 
-    python scripts/experiments.py [--out profiles/r01_experiments]
+    python tests/tools/experiments.py [--out profiles/r01_experiments]
 
 1. l-sweep (Fig. 2 "exponential run time with the increase of
    the motif length"): search-kernel time for l = 9..16 at d = 3, n=20, t=600,
@@ -23,7 +23,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import fmgen  # noqa: E402
@@ -125,7 +125,7 @@ def main():
 
     json.dump(res, open(args.out + ".json", "w"), indent=1)
     # Table II layout
-    lines = [f"# Paper-experiment analogues on B200 (scripts/experiments.py --algo {args.algo})", "",
+    lines = [f"# Paper-experiment analogues on B200 (tests/tools/experiments.py --algo {args.algo})", "",
              "## Fig. 2 analogue: search-kernel time vs l (d = 3, n=20, t=600, seed 1)", "",
              "| l | kernel ms | ratio to l-1 | candidates/s | motifs |", "|---|---|---|---|---|"]
     for r in res["lsweep"]:

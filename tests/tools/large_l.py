@@ -4,7 +4,7 @@ like the paper's challenge problem (n=20, t=600) at larger (l, d):
 exhaustive 4^l enumeration on one B200, planted-consensus recovery, and an
 oracle spot check on a code range around the consensus (oracle_find64).
 
-    python scripts/large_l.py [--configs 17,6 18,6 19,7] [--budget-s 60]
+    python tests/tools/large_l.py [--configs 17,6 18,6 19,7] [--budget-s 60]
 """
 from __future__ import annotations
 
@@ -14,7 +14,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import fmgen  # noqa: E402

@@ -3,14 +3,14 @@ both kernel families, shared-memory and global tables, ranges, both block
 sizes, the no-skip variants and an invalid byte -- each result checked against
 the oracle.  Usage on the GPU box (one tool per call):
 
-    compute-sanitizer --tool memcheck --error-exitcode 9 python scripts/sanitize_case.py
+    compute-sanitizer --tool memcheck --error-exitcode 9 python tests/tools/sanitize_case.py
 """
 from __future__ import annotations
 
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import fmgen  # noqa: E402

@@ -2,7 +2,7 @@
 """Randomised parity stress (GPU box): random shapes, (l, d), families, block
 sizes, launch knobs and code ranges against the CPU oracle, bit for bit.
 
-    python scripts/stress_parity.py [--seconds 240] [--seed 1]
+    python tests/tools/stress_parity.py [--seconds 240] [--seed 1]
 
 Covers corners the fixed tests sample sparsely: W not a multiple of 32, the
 streaming (NW = 0) path for W > 1536, many sequences, d near l, l > 16 on
@@ -17,7 +17,7 @@ import random
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import fmgen  # noqa: E402
