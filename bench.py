@@ -199,8 +199,9 @@ def run_gpu(args) -> int:
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.Stream(device=dev)
-    algo = {"auto": pms.ALGO_AUTO, "candidate": pms.ALGO_CANDIDATE, "block": pms.ALGO_BLOCK}[args.algo]
-    plan = pms.Plan(n, t, l, d, pms.Launch(algo=algo))
+    algo = {"auto": pms.ALGO_AUTO, "candidate": pms.ALGO_CANDIDATE, "block": pms.ALGO_BLOCK,
+            "slice": pms.ALGO_SLICE}[args.algo]
+    plan = pms.Plan(n, t, l, d, pms.Launch(algo=algo, block_digits=args.block_digits))
     total = 4 ** l
     from paper_1403_1313_b200.shard import shard_range
     lo, hi = shard_range(total, rank, world) if strong else (0, total)
@@ -451,7 +452,9 @@ def main() -> int:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--algo", choices=["auto", "candidate", "block"], default="auto")
+    ap.add_argument("--algo", choices=["auto", "candidate", "block", "slice"], default="auto")
+    ap.add_argument("--block-digits", type=int, default=0,
+                    help="pms_launch.block_digits (0 = automatic)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: an instance per rank; strong: one instance sharded by candidate range")
     ap.add_argument("--candidate-steps", type=int, default=3,

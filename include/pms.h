@@ -97,8 +97,16 @@ typedef struct pms_launch {
  *     0, 1, ... and dropped at the first sequence with no window within d; the
  *     block is abandoned when no candidate is left (the skip rule on 4^S
  *     candidates at once).  Needs l >= 5 (else the candidate family runs).
- *   PMS_ALGO_AUTO (0): PMS_ALGO_BLOCK when l >= 5, else PMS_ALGO_CANDIDATE. */
-enum { PMS_ALGO_AUTO = 0, PMS_ALGO_CANDIDATE = 1, PMS_ALGO_BLOCK = 2 };
+ *   PMS_ALGO_SLICE: the block family's computation (same blocks, same
+ *     per-candidate skip rule, same set) with the prefix test bit-sliced over
+ *     windows (a lane's 32 windows at once: one-hot base planes of the prefix
+ *     positions summed by a carry-save adder tree, no per-window POPC) and
+ *     the hits resolved in batches through per-warp queues.
+ *     Applies to l <= 16, t - l + 1 <= 1024 and d < l - S; elsewhere a
+ *     request for it runs PMS_ALGO_BLOCK.
+ *   PMS_ALGO_AUTO (0): PMS_ALGO_SLICE where it applies, else PMS_ALGO_BLOCK
+ *     when l >= 5, else PMS_ALGO_CANDIDATE. */
+enum { PMS_ALGO_AUTO = 0, PMS_ALGO_CANDIDATE = 1, PMS_ALGO_BLOCK = 2, PMS_ALGO_SLICE = 3 };
 
 /* Counters and timings of the last execution of a plan. */
 typedef struct pms_stats {

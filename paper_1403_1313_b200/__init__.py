@@ -18,7 +18,7 @@ import numpy as np
 from ._build import LIB, build
 
 OK, E_ARG, E_CHAR, E_TOO_LARGE, E_CUDA, E_TRUNCATED = 0, -1, -2, -3, -4, -5
-ALGO_AUTO, ALGO_CANDIDATE, ALGO_BLOCK = 0, 1, 2
+ALGO_AUTO, ALGO_CANDIDATE, ALGO_BLOCK, ALGO_SLICE = 0, 1, 2, 3
 MAX_L = 16     # uint32 codes (pms_find, pms_find_ex, pms_plan_execute)
 MAX_L64 = 31   # uint64 codes (pms_find64, pms_find64_ex, pms_plan_execute64)
 
@@ -135,7 +135,7 @@ def _rows(seqs) -> np.ndarray:
 @dataclass
 class FindResult:
     status: int
-    codes: np.ndarray   # uint32 ascending (valid when status == OK)
+    codes: np.ndarray   # ascending codes when status == OK, else empty
     count: int          # exact number of motifs
     stats: Stats | None = None
 
@@ -153,7 +153,9 @@ def _find_ex(fname, ctype, seqs, l, d, lo, hi, launch, max_out, want_stats) -> F
                                  ctypes.byref(launch) if launch else None, out.ctypes.data,
                                  int(max_out), ctypes.byref(cnt),
                                  ctypes.byref(st) if st is not None else None)
-    k = min(int(cnt.value), int(max_out)) if status in (OK, E_TRUNCATED) else 0
+    # codes are defined only on OK (include/pms.h: on PMS_E_TRUNCATED the
+    # caller's buffer is unspecified, so nothing of it is returned)
+    k = int(cnt.value) if status == OK else 0
     return FindResult(status, out[:k].copy(), int(cnt.value), st)
 
 

@@ -31,6 +31,7 @@
 #include "pms.h"
 #include "pms_device.cuh"
 #include "pms_kernels.cuh"
+#include "pms_slice.cuh"
 
 namespace pms {  // defined in pms64.cu
 const BlockKernel* block_kernels64(int* count);
@@ -144,6 +145,27 @@ const BlockKernel kBlockKernels[] = {
     {6, 0, pms_search_block<Bp32, 6, true, 0>, pms_search_block<Bp32, 6, false, 0>},
     PMS_NWB_LIST(PMS_BLK5) PMS_NWB_LIST(PMS_BLK6)};
 
+// PMS_ALGO_SLICE instances: block digits S x prefix length LP = l - S
+// (l <= 16), table staged in shared memory or read through L1/L2
+struct SliceKernel {
+    int S, LP;
+    SliceFn fn_smem, fn_global;
+};
+#define PMS_SLICE(S, LP) {S, LP, pms_search_slice<S, LP, true>, pms_search_slice<S, LP, false>},
+#define PMS_SLICE5(LP) PMS_SLICE(5, LP)
+#define PMS_SLICE6(LP) PMS_SLICE(6, LP)
+#define PMS_SLICE7(LP) PMS_SLICE(7, LP)
+#define PMS_LP_LIST(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9)
+const SliceKernel kSliceKernels[] = {PMS_LP_LIST(PMS_SLICE5) PMS_SLICE5(10) PMS_SLICE5(11)
+                                     PMS_LP_LIST(PMS_SLICE6) PMS_SLICE6(10)
+                                     PMS_LP_LIST(PMS_SLICE7)};
+
+const SliceKernel* find_slice_kernel(int S, int LP) {
+    for (const SliceKernel& k : kSliceKernels)
+        if (k.S == S && k.LP == LP) return &k;
+    return nullptr;
+}
+
 // ---------------------------------------------------- roofline microbenchmark
 // The exact per-compare sequence of pms_search_reg<G,NW> (same register-
 // resident windows, same candidate generation, same vote), with no early exit
@@ -238,6 +260,41 @@ const uint32_t* ensure_ball_table(int dev) {
     return g_ball[dev];
 }
 
+// The slice family's ball table (pms_slice.cuh): the rows of T, then the
+// 16-word radius-1 rows R1[e][u].  Once per device, like g_ball.
+uint32_t* g_sball[64] = {nullptr};
+
+const uint32_t* ensure_slice_ball_table(int dev) {
+    std::lock_guard<std::mutex> lk(g_ball_mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!g_sball[dev]) {
+        std::vector<uint32_t> h(kSTWords, 0u);
+        for (int idx = 0; idx < kSR1Off; ++idx) {
+            const uint32_t m = idx & 31u, e = (idx >> 5) & 31u;
+            const int rho = idx >> 10;
+            uint32_t w = 0;
+            for (uint32_t b = 0; b < 32; ++b)
+                if (__builtin_popcount(m | (b ^ e)) <= rho) w |= 1u << b;
+            h[idx] = w;
+        }
+        for (int e = 0; e < 32; ++e) {
+            uint32_t* r = &h[kSR1Off + e * 16];
+            r[0] = h[1024 + e * 32 + 0];
+            for (int q = 0; q < 5; ++q) r[1 + q] = h[1024 + e * 32 + (1 << q)];
+            for (int u = 6; u < 15; ++u) r[u] = 1u << e;
+        }
+        uint32_t* d = nullptr;
+        if (cudaMalloc(&d, kSTWords * 4) != cudaSuccess) return nullptr;
+        if (cudaMemcpy(d, h.data(), kSTWords * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {
+            cudaFree(d);
+            return nullptr;
+        }
+        g_sball[dev] = d;
+    }
+    return g_sball[dev];
+}
+
 int ensure_constants() {
     static thread_local int dev_done[64] = {0};
     int dev = 0;
@@ -275,6 +332,12 @@ struct pms_plan {
     int grid = 0, block = kBlock, batch = kSub;
     unsigned long long last_lo = 0, last_hi = 0;
     bool executed = false;
+    // PMS_ALGO_SLICE (pms_slice.cuh): match planes, r = 0 slots, kernel
+    void* d_planes = nullptr;
+    void* d_slots = nullptr;
+    int NWl = 0, LP = 0;
+    uint32_t plane_bytes = 0, slot_bytes = 0;
+    SliceFn sfn = nullptr;
 };
 
 namespace {
@@ -291,6 +354,8 @@ int check_shape(int32_t n, int32_t t, int32_t l, int32_t d, int32_t max_l) {
 void destroy_plan(pms_plan* p) {
     if (!p) return;
     cudaFree(p->d_table);
+    cudaFree(p->d_planes);
+    cudaFree(p->d_slots);
     if (!p->state_external) cudaFree(p->d_state);
     cudaFreeHost(p->h_state);
     for (cudaEvent_t e : p->ev)
@@ -333,13 +398,84 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     // block family: AUTO or explicit; with no_skip only when asked for explicitly
     // (AUTO + no_skip keeps the per-candidate plain brute force)
     const bool block_algo =
-        (p->launch.algo == PMS_ALGO_BLOCK || (p->launch.algo == PMS_ALGO_AUTO && !p->launch.no_skip)) &&
+        (p->launch.algo == PMS_ALGO_BLOCK || p->launch.algo == PMS_ALGO_SLICE ||
+         (p->launch.algo == PMS_ALGO_AUTO && !p->launch.no_skip)) &&
         l >= kBlkMinL;
     // block digits S: 6 (4096-candidate blocks) when there are enough blocks to
     // keep every warp busy (l >= 13: >= 16k blocks), else 5
     int S = p->launch.block_digits == 5 || p->launch.block_digits == 6 ? p->launch.block_digits
                                                                         : (l >= 13 ? 6 : 5);
     if (S > l) S = 5;
+    // S = 7 (16384-candidate blocks) exists in the slice family only
+    const int S_slice = p->launch.block_digits == 7 ? 7 : S;
+    // PMS_ALGO_SLICE (the default where it applies): 32-bit codes, rows of at
+    // most 1024 windows, a prefix of 1..11 digits with d below its length
+    // (otherwise every window would hit); elsewhere the block family runs
+    if (block_algo && p->launch.algo != PMS_ALGO_BLOCK && !p->wide && p->W <= 1024 &&
+        l - S_slice >= 1 && d < l - S_slice && find_slice_kernel(S_slice, l - S_slice)) {
+        S = S_slice;
+        const SliceKernel* sk = find_slice_kernel(S, l - S);
+        p->algo = PMS_ALGO_SLICE;
+        p->S = S;
+        p->LP = l - S;
+        p->NWl = (p->W + 31) / 32;
+        p->Wp = 32 * p->NWl;
+        p->tab_bytes = (uint32_t)((size_t)n * p->Wp * 4);
+        p->plane_bytes = (uint32_t)((size_t)n * p->LP * 512);
+        p->slot_bytes = (uint32_t)(((size_t)n * p->Wp * 2 + 15) / 16 * 16);
+        cudaFuncAttributes fs{};
+        if (cudaFuncGetAttributes(&fs, (const void*)sk->fn_smem) != cudaSuccess) {
+            destroy_plan(p);
+            return fail_cuda(__LINE__);
+        }
+        // ball table + per-warp words and queues (SliceCfg<S>::kWorkBytes)
+        const size_t ball_bytes = S == 5 ? SliceCfg<5>::kWorkBytes
+                                  : S == 6 ? SliceCfg<6>::kWorkBytes : SliceCfg<7>::kWorkBytes;
+        p->in_smem = !p->launch.table_global &&
+                     ball_bytes + p->plane_bytes + p->slot_bytes + fs.sharedSizeBytes <= (size_t)smem_optin;
+        p->smem_bytes = (uint32_t)ball_bytes + (p->in_smem ? p->plane_bytes + p->slot_bytes : 0u);
+        p->sfn = p->in_smem ? sk->fn_smem : sk->fn_global;
+        p->G = 32; p->NW = p->NWl; p->generic = 0;
+        p->block = S == 7 ? SliceCfg<7>::NT : SliceCfg<6>::NT;
+        p->d_ball = ensure_slice_ball_table(p->dev);
+        cudaFuncAttributes fa{};
+        int occ = 0;
+        if (!p->d_ball || cudaFuncGetAttributes(&fa, (const void*)p->sfn) != cudaSuccess ||
+            p->smem_bytes + fa.sharedSizeBytes > (size_t)smem_optin ||
+            cudaFuncSetAttribute((const void*)p->sfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_optin - (int)fa.sharedSizeBytes) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->sfn, p->block,
+                                                          p->smem_bytes) != cudaSuccess ||
+            occ < 1) {
+            destroy_plan(p);
+            return fail_cuda(__LINE__);
+        }
+        if (p->launch.ctas_per_sm > 0) occ = std::min(occ, (int)p->launch.ctas_per_sm);
+        p->grid = p->sms * occ;
+        if (p->launch.grid_ctas > 0) p->grid = std::min((int)p->launch.grid_ctas, p->grid);
+        if (cudaMalloc(&p->d_table, p->tab_bytes) != cudaSuccess ||
+            cudaMalloc(&p->d_planes, p->plane_bytes) != cudaSuccess ||
+            cudaMalloc(&p->d_slots, p->slot_bytes) != cudaSuccess ||
+            cudaMalloc(&p->d_state, sizeof(DevState)) != cudaSuccess ||
+            cudaMallocHost(&p->h_state, sizeof(DevState)) != cudaSuccess ||
+            cudaMemset(p->d_state, 0, sizeof(DevState)) != cudaSuccess ||
+            cudaMemset(p->d_slots, 0, p->slot_bytes) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {
+            destroy_plan(p);
+            return fail_cuda(__LINE__);
+        }
+        for (cudaEvent_t& e : p->ev)
+            if (cudaEventCreate(&e) != cudaSuccess) {
+                destroy_plan(p);
+                return fail_cuda(__LINE__);
+            }
+        if (cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking) != cudaSuccess) {
+            destroy_plan(p);
+            return fail_cuda(__LINE__);
+        }
+        *plan = p;
+        return PMS_OK;
+    }
     const BlockKernel* bk = nullptr;
     if (block_algo) {
         for (int q = 0; q < nbk; ++q)  // generic (NW = 0) of this S first
@@ -475,8 +611,9 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // batches and lo are aligned to the plan's unit: one block (4^S candidates)
     // for the block family, a 256-candidate sub-block for the candidate family
-    const unsigned long long kUnit =
-        p->algo == PMS_ALGO_BLOCK ? (1ull << (2 * p->S)) : (unsigned long long)kSub;
+    const unsigned long long kUnit = (p->algo == PMS_ALGO_BLOCK || p->algo == PMS_ALGO_SLICE)
+                                         ? (1ull << (2 * p->S))
+                                         : (unsigned long long)kSub;
     const unsigned long long lo_al = lo / kUnit * kUnit;
     const unsigned long long span = hi - lo_al;
 
@@ -506,6 +643,52 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     a.ball = p->d_ball;
     if (++p->epoch == 0) p->epoch = 1;  // 0 is the reset value of st->bad
     a.epoch = p->epoch;
+    static const bool no_pdl = std::getenv("PMS_NO_PDL") != nullptr;
+    if (p->algo == PMS_ALGO_SLICE) {
+        SliceArgs sa{};
+        sa.planes = static_cast<const uint32_t*>(p->d_planes);
+        sa.slots = static_cast<const uint16_t*>(p->d_slots);
+        sa.words = static_cast<const uint32_t*>(p->d_table);
+        sa.ball = p->d_ball;
+        sa.n = p->n; sa.W = p->W; sa.Wp = p->Wp; sa.NWl = p->NWl;
+        sa.dp = (uint32_t)std::min(p->d, p->l);
+        const uint32_t K = 16u - (uint32_t)(p->LP - p->d);  // 1 <= LP - d <= LP
+        for (int b = 0; b < 4; ++b) sa.kmask[b] = ((K >> b) & 1u) ? 0xFFFFFFFFu : 0u;
+        sa.lo = lo; sa.hi = hi; sa.lo_al = lo_al; sa.span = span; sa.batch = batch;
+        sa.skip = p->launch.no_skip ? 0 : 1;
+        sa.handoff = p->launch.handoff > 0 ? p->launch.handoff : (p->d >= 5 ? 2 : 1);
+        sa.out_wide = out_wide;
+        sa.plane_bytes = p->plane_bytes; sa.slot_bytes = p->slot_bytes;
+        sa.st = p->d_state; sa.epoch = p->epoch;
+        sa.nout = reinterpret_cast<unsigned long long*>(d_count);
+        sa.out = d_out; sa.cap = cap;
+        if (cudaEventRecord(p->ev[0], s) != cudaSuccess) return fail_cuda(__LINE__);
+        auto pack = p->S == 5 ? pms_pack_slice<5> : p->S == 6 ? pms_pack_slice<6> : pms_pack_slice<7>;
+        pack<<<(unsigned)p->n, kSlicePackThreads, 0, s>>>(
+            d_seqs, p->n, p->t, p->l, p->W, p->NWl, p->LP, static_cast<uint32_t*>(p->d_planes),
+            static_cast<uint16_t*>(p->d_slots), static_cast<uint32_t*>(p->d_table), p->d_state,
+            reinterpret_cast<unsigned long long*>(d_count), p->epoch);
+        const cudaError_t e_pack = cudaGetLastError();
+        if (e_pack != cudaSuccess) return fail_cuda(__LINE__, e_pack);
+        if (timed && cudaEventRecord(p->ev[1], s) != cudaSuccess) return fail_cuda(__LINE__);
+        if (span > 0) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)p->grid);
+            cfg.blockDim = dim3((unsigned)p->block);
+            cfg.dynamicSmemBytes = (size_t)p->smem_bytes;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = no_pdl ? 0 : 1;
+            const cudaError_t e = cudaLaunchKernelEx(&cfg, p->sfn, sa);
+            if (e != cudaSuccess) return fail_cuda(__LINE__, e);
+        }
+        if (cudaEventRecord(p->ev[2], s) != cudaSuccess) return fail_cuda(__LINE__);
+        p->executed = true;
+        return PMS_OK;
+    }
 
     // device work of a step: pre-pass (which also resets the state and the
     // result counter), search; the state read-back is pms_plan_wait's
@@ -520,7 +703,6 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     if (timed && cudaEventRecord(p->ev[1], s) != cudaSuccess) return fail_cuda(__LINE__);
     if (span > 0) {
         // programmatic dependent launch after the pre-pass (PMS_NO_PDL: plain)
-        static const bool no_pdl = std::getenv("PMS_NO_PDL") != nullptr;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)p->grid);
         cfg.blockDim = dim3((unsigned)p->block);

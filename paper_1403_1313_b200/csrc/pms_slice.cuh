@@ -1,0 +1,578 @@
+// pms_slice.cuh -- PMS_ALGO_SLICE: the block family with a bit-sliced pass 1
+// and batched hit resolution (32-bit codes, l <= 16).  DESIGN.md section 6c.
+//
+// What it computes is exactly what pms_search_block computes (PAPER.md:63
+// skip-BF, per candidate, sequences in input order): the 4^S candidates of a
+// block share their first LP = l - S digits (the prefix P); for a window w with
+// prefix distance p = Hamming(P, w[0..LP)) <= d, the block candidates that
+// match w are the suffixes within r = d - p of w's suffix (Hamming distance is
+// additive over positions).  Only the mapping onto the machine differs:
+//
+// pass 1, bit-sliced over windows.  Lane L owns the NWl = ceil(W/32)
+//   consecutive windows k = L*NWl + q (bit q of its words).  The pre-pass
+//   stores, per (sequence i, prefix position j, base b, lane L), the 32-bit
+//   "match plane" whose bit q says window L*NWl+q has base b at position j.
+//   A block's prefix digits b_j pick one plane per position, so the lane
+//   loads LP words (one conflict-free 128-B row per warp each) and adds the LP
+//   match bits of all its windows at once with a carry-save adder tree
+//   (2 LOP3 per full adder) into a 5-bit counter preloaded with K = 16 - T,
+//   T = LP - d: bit 4 of K + matches is "matches >= T", i.e. p <= d (a hit),
+//   and the low four bits are then r = d - p.  No POPC, no per-window work.
+//
+// pass 2, batched.  The measured cost of a shared-memory atomic is ~4 SM
+//   cycles per warp instruction whatever the number of active lanes
+//   (tests/tools/ubench_smem.cu), so hits are resolved full-width instead of
+//   by divergent per-lane loops:
+//   * r = 0 hits (the window's own suffix only) and r = 1 hits (the radius-1
+//     ball, 6 + 3X words) are appended, as precomputed 12-bit slots
+//     (word * 32 + bit of the window's suffix in the block's mask), to two
+//     per-warp queues; one shared atomicAdd claims both queue positions;
+//   * r = 0 queue: 32 hits per atomic instruction;
+//   * r = 1 queue: lane L applies update u = L mod NU of hit L / NU (NU =
+//     6 + 3X words per ball; 3 hits per instruction at S = 6): word
+//     slot/32 XOR a per-lane constant, bits from a 16-entry row per e;
+//   * r >= 2 hits (rare): broadcast to all lanes, which read their own words'
+//     bits from the ball table T[r][e][m] (as pms_search_block).
+//   A queue overflow (possible only when hits are dense: small LP, large d)
+//   resolves that scan with per-lane atomics instead; results are the same.
+//
+// The candidate mask words are word-major (word k of lane L at k*32 + L), so
+// a lane's words, the ball-table broadcast atomics and the end-of-scan reads
+// are bank-conflict-free.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pms_device.cuh"
+#include "pms_kernels.cuh"
+
+namespace pms {
+
+struct SliceArgs {
+    const uint32_t* planes;   // [n][LP][4][32] match planes (global)
+    const uint16_t* slots;    // [n][Wp] r = 0 slot of each window (global)
+    const uint32_t* words;    // [n][Wp] packed Bp32 windows (hand-off checks, global)
+    const uint32_t* ball;     // slice ball table (kSTWords words, global)
+    int n, W, Wp, NWl;        // Wp = 32 * NWl
+    uint32_t dp;              // min(d, l)
+    uint32_t kmask[4];        // bits of K = 16 - (LP - d) as 0 / ~0 masks
+    unsigned long long lo, hi, lo_al, span;
+    int batch, skip, handoff;
+    int out_wide;
+    uint32_t plane_bytes, slot_bytes;  // staged sizes (16-B multiples)
+    DevState* st;
+    uint32_t epoch;
+    unsigned long long* nout;
+    void* out;
+    unsigned long long cap;
+};
+
+using SliceFn = void (*)(SliceArgs);
+
+// Slice ball table: T[rho][e][m] (rho = 0..6, as pms_search_block's) then the
+// radius-1 rows R1[e][u] (16 words per e): u = 0: T[1][e][0]; u = 1..5:
+// T[1][e][1 << (u-1)]; u = 6..14: 1 << e (the centre bit, for the words one
+// upper position away); 15: 0.
+constexpr int kSR1Off = 7 * 1024;
+constexpr int kSTWords = kSR1Off + 32 * 16;  // 30 KB
+constexpr int kSliceCap0 = 256;              // per-warp r = 0 queue entries (u16 slots)
+constexpr int kSliceCap1 = 128;              // per-warp r = 1 queue entries (u16 slots)
+constexpr int kSliceCap2 = 64;               // per-warp r >= 2 queue entries (slot | r << 16)
+constexpr int kSliceMaxLP = 11;              // l <= 16, S >= 5
+constexpr int kSlicePackThreads = 256;
+
+// Per block size: S = 5, 6 run 32 warps per SM (64 registers); S = 7 (16
+// words per lane) runs 16 warps with 128 registers.
+template <int S>
+struct SliceCfg {
+    static constexpr int X = S - 5;
+    static constexpr int KW = 1 << (2 * X);   // mask words per lane
+    static constexpr int NU = 6 + 3 * X;      // words of a radius-1 ball
+    static constexpr int HPR = 32 / NU;       // r = 1 hits per round
+    static constexpr int NT = S >= 7 ? 512 : 1024;
+    static constexpr int NWARP = NT / 32;
+    // dynamic shared memory in front of the staged tables: [ball table]
+    // [per-warp candidate words][r = 0 / 1 queues][r >= 2 queues]; the word
+    // blocks start at a multiple of their size (30 KB = 15 x 2 KB)
+    static constexpr uint32_t kAccAlign = 32u * KW * 4u;  // one warp's word block
+    static constexpr uint32_t kAccOff = kSTWords * 4u;     // (+ up to kAccAlign - 1 at run time)
+    static constexpr uint32_t kAccBytes = NWARP * 32u * KW * 4u + kAccAlign;
+    static constexpr uint32_t kQ01Off = kAccOff + kAccBytes;
+    static constexpr uint32_t kQ2Off = kQ01Off + NWARP * (kSliceCap0 + kSliceCap1) * 2u;
+    static constexpr uint32_t kWorkBytes = kQ2Off + NWARP * kSliceCap2 * 4u;  // = planes offset
+    static_assert(kWorkBytes % 128u == 0, "TMA destinations");
+};
+
+}  // namespace pms
+
+namespace {
+
+using namespace pms;
+
+// ------------------------------------------------------------- pre-pass
+// One CTA per sequence i (W <= 1024): stage the row's 2-bit codes in shared
+// memory (checking every byte once, PAPER.md:63 windows are substrings of
+// the input), then write (1) the packed Bp32 window words (rows padded to Wp
+// with copies of window W-1), (2) each window's r = 0 slot for block digits
+// S, (3) the LP x 4 x 32 match planes of the prefix positions.  Thread 0 of
+// CTA 0 resets the step's state and the result counter (no memset launch).
+template <int S>
+__global__ void __launch_bounds__(kSlicePackThreads) pms_pack_slice(
+    const uint8_t* __restrict__ seqs, int n, int t, int l, int W, int NWl, int LP,
+    uint32_t* __restrict__ planes, uint16_t* __restrict__ slots, uint32_t* __restrict__ words,
+    DevState* st, unsigned long long* nout, uint32_t epoch) {
+    constexpr int X = S - 5;
+    __shared__ uint8_t code[1024 + 32];
+    pdl_launch_dependents();
+    const int i = blockIdx.x;
+    if (i == 0 && threadIdx.x == 0) {
+        *nout = 0ull;
+        st->next = 0ull;
+        st->extra = 0ull;
+        st->block_scans = 0ull;
+    }
+    if (i >= n) return;
+    const int Wp = 32 * NWl;
+    const uint8_t* row = seqs + (long long)i * t;
+    PMS_CHECK(t <= 1024 + 32);
+    uint32_t bad = 0;
+    for (int b = threadIdx.x; b < t; b += kSlicePackThreads) {
+        const uint32_t u = row[b] & 0xDFu;  // upper-case; only 'x'/'X' map to 'X'
+        const uint32_t c = u == 'A' ? 0u : u == 'C' ? 1u : u == 'G' ? 2u : u == 'T' ? 3u : 4u;
+        bad |= c >> 2;
+        code[b] = (uint8_t)c;
+    }
+    if (bad) *(volatile unsigned int*)&st->bad = epoch;
+    __syncthreads();
+    for (int k = threadIdx.x; k < Wp; k += kSlicePackThreads) {
+        const int src = min(k, W - 1);
+        uint32_t H = 0, L = 0;
+        for (int j = 0; j < l; ++j) {
+            const uint32_t c = code[src + j] & 3u;
+            H = (H << 1) | (c >> 1);
+            L = (L << 1) | (c & 1u);
+        }
+        words[(long long)i * Wp + k] = (H << 16) | L;
+        const uint32_t eH = H & ((1u << S) - 1u), eL = L & ((1u << S) - 1u);
+        const uint32_t kw = ((eH >> 5) << X) | (eL >> 5);
+        slots[(long long)i * Wp + k] = (uint16_t)(k < W ? ((kw * 32u + (eH & 31u)) * 32u + (eL & 31u)) : 0u);
+    }
+    for (int idx = threadIdx.x; idx < LP * 128; idx += kSlicePackThreads) {
+        const int j = idx >> 7, b = (idx >> 5) & 3, ln = idx & 31;
+        uint32_t v = 0;
+        for (int q = 0; q < NWl; ++q) {
+            const int k = ln * NWl + q;
+            if (k < W && code[k + j] == (uint8_t)b) v |= 1u << q;
+        }
+        planes[(long long)i * LP * 128 + idx] = v;
+    }
+}
+
+// ----------------------------------------------------- carry-save counting
+// Reduce N equal-weight bit planes to one (their sum mod 2); the carries
+// (weight x2, N/2 of them) go to cy[0..N/2).  Full adder: sum = a^b^c (one
+// LOP3), carry = maj(a,b,c) (one LOP3).
+template <int N>
+__device__ __forceinline__ uint32_t csa_col(uint32_t* v, uint32_t* cy) {
+    if constexpr (N == 0) {
+        return 0u;
+    } else if constexpr (N == 1) {
+        return v[0];
+    } else if constexpr (N == 2) {
+        cy[0] = v[0] & v[1];
+        return v[0] ^ v[1];
+    } else {
+        const uint32_t a = v[0], b = v[1], c = v[2];
+        cy[0] = (a & b) | (c & (a ^ b));
+        v[2] = a ^ b ^ c;  // the sum joins the column again (queue order: balanced depth)
+        return csa_col<N - 2>(v + 2, cy + 1);
+    }
+}
+
+// K + (number of set planes among m[0..LP)) as five bit planes c[0..4],
+// K given by its four bit masks (K <= 15, LP <= 11: the total is < 32).
+template <int LP>
+__device__ __forceinline__ void slice_count(const uint32_t (&m)[LP], const uint32_t (&k)[4],
+                                            uint32_t (&c)[5]) {
+    constexpr int N0 = LP + 1, C0 = N0 / 2;
+    constexpr int N1 = C0 + 1, C1 = N1 / 2;
+    constexpr int N2 = C1 + 1, C2 = N2 / 2;
+    constexpr int N3 = C2 + 1, C3 = N3 / 2;
+    uint32_t v0[N0], y0[C0 > 0 ? C0 : 1];
+#pragma unroll
+    for (int j = 0; j < LP; ++j) v0[j] = m[j];
+    v0[LP] = k[0];
+    c[0] = csa_col<N0>(v0, y0);
+    uint32_t v1[N1], y1[C1 > 0 ? C1 : 1];
+#pragma unroll
+    for (int j = 0; j < C0; ++j) v1[j] = y0[j];
+    v1[C0] = k[1];
+    c[1] = csa_col<N1>(v1, y1);
+    uint32_t v2[N2], y2[C2 > 0 ? C2 : 1];
+#pragma unroll
+    for (int j = 0; j < C1; ++j) v2[j] = y1[j];
+    v2[C1] = k[2];
+    c[2] = csa_col<N2>(v2, y2);
+    uint32_t v3[N3], y3[C3 > 0 ? C3 : 1];
+#pragma unroll
+    for (int j = 0; j < C2; ++j) v3[j] = y2[j];
+    v3[C2] = k[3];
+    c[3] = csa_col<N3>(v3, y3);
+    uint32_t top = 0u;  // weight 16: at most one of these can be set (total < 32)
+#pragma unroll
+    for (int j = 0; j < C3; ++j) top |= y3[j];
+    c[4] = top;
+}
+
+
+// ------------------------------------------------------ shared-space access
+// 32-bit shared-window addresses and explicit ld/st/red.shared: the compiler
+// otherwise re-derives generic->shared bases inside the hit loops.
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_or(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add(uint32_t a, uint32_t v) {
+    uint32_t r;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
+    return r;
+}
+
+// r = d - p of the hit at bit q (the low four counter planes)
+__device__ __forceinline__ uint32_t slice_r(const uint32_t (&c)[5], int q) {
+    return ((c[0] >> q) & 1u) | (((c[1] >> q) & 1u) << 1) | (((c[2] >> q) & 1u) << 2) |
+           (((c[3] >> q) & 1u) << 3);
+}
+
+// Word delta (word index = k * 32 + lane) of update u of a radius-1 ball:
+// u = 0 the hit's own word, u = 1..5 the lanes one H bit away, u = 6.. the
+// words one upper suffix position away (L bit, H bit, both).
+template <int X>
+__device__ __forceinline__ uint32_t r1_delta(uint32_t u) {
+    if (u == 0) return 0u;
+    if (u <= 5) return 1u << (u - 1);
+    const uint32_t v = u - 6, pos = v / 3, alt = v % 3;
+    const uint32_t kd = alt == 0 ? (1u << pos) : alt == 1 ? (1u << (X + pos)) : ((1u << pos) | (1u << (X + pos)));
+    return kd * 32u;
+}
+
+// One r >= 2 hit (slot, r) applied by every lane to its own words: word ek
+// gets T[r][el5][lane ^ eh5]; with X >= 1 the words one upper position away
+// get T[r-1] and -- via `common`, ORed into every word at the end of the scan
+// -- all words get T[r-X] (a superset-free bound: T[r-X] is within budget
+// wherever X upper positions mismatch).
+template <int X>
+__device__ __forceinline__ void slice_bcast(uint32_t slot, uint32_t r, uint32_t lane, uint32_t T_s,
+                                            uint32_t acc_s, uint32_t& common) {
+    // (radius >= 5 covers all five positions: row 6 is all ones)
+    const uint32_t el5 = slot & 31u, eh5 = (slot >> 5) & 31u, ek = slot >> 10;
+    const uint32_t toff = T_s + ((el5 << 5) | (lane ^ eh5)) * 4u;
+    const uint32_t aw = acc_s + (ek * 32u + lane) * 4u;
+    red_or(aw, lds32(toff + min(r, 6u) * 4096u));
+    if constexpr (X >= 1) common |= lds32(toff + min(r - (uint32_t)X, 6u) * 4096u);
+    if constexpr (X >= 2) {
+        const uint32_t b = lds32(toff + min(r - 1u, 6u) * 4096u);
+#pragma unroll
+        for (int u = 0; u < 3 * X; ++u) red_or(aw ^ (r1_delta<X>(6u + (uint32_t)u) * 4u), b);
+    }
+}
+
+// ------------------------------------------------------------ the search
+template <int S, int LP, bool SMEM>
+__global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs a) {
+    using B = BlkTraits<S>;
+    using C = SliceCfg<S>;
+    constexpr int X = C::X, KW = C::KW, NU = C::NU, HPR = C::HPR, NWARP = C::NWARP;
+    static_assert(LP >= 1 && LP <= kSliceMaxLP, "prefix length");
+    // [ball table][candidate words][queues][planes][slots] (SliceCfg); each
+    // warp's word block is aligned to its size, so a word index XOR is an
+    // address XOR (r = 1 rounds)
+    // (only 128-B alignment of the dynamic window is real -- measured base
+    // 0xC00 -- so nothing larger is declared: the compiler would fold it)
+    extern __shared__ __align__(128) uint32_t sdyn[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t qcnts[NWARP];
+    pdl_wait();
+    if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const uint32_t dyn_s = smem_u32(sdyn);
+    // word blocks aligned to their size at run time (the dynamic window's
+    // base alignment is not guaranteed beyond 128 B)
+    const uint32_t acc0_s = (dyn_s + C::kAccOff + C::kAccAlign - 1u) & ~(C::kAccAlign - 1u);
+    const uint32_t acc_s = acc0_s + wid * C::kAccAlign;
+    const uint32_t q0_s = dyn_s + C::kQ01Off + wid * ((kSliceCap0 + kSliceCap1) * 2u);
+    const uint32_t q1_s = q0_s + 2u * kSliceCap0;
+    const uint32_t q2_s = dyn_s + C::kQ2Off + wid * (kSliceCap2 * 4u);
+    const uint32_t qc_s = smem_u32(&qcnts[wid]);
+    PMS_CHECK((acc_s & (32u * KW * 4u - 1u)) == 0u);
+#pragma unroll
+    for (int k = 0; k < KW; ++k) sts32(acc_s + (k * 32u + lane) * 4u, 0u);
+    if (lane == 0) sts32(qc_s, 0u);
+    uint32_t* splanes = sdyn + C::kWorkBytes / 4u;
+    uint16_t* sslots = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(splanes) + a.plane_bytes);
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&bar, kSTWords * 4u + (SMEM ? a.plane_bytes + a.slot_bytes : 0u));
+        tma_bulk_g2s(sdyn, a.ball, kSTWords * 4u, &bar);
+        if (SMEM) {
+            for (uint32_t off = 0; off < a.plane_bytes; off += 65536u)
+                tma_bulk_g2s(reinterpret_cast<char*>(splanes) + off,
+                             reinterpret_cast<const char*>(a.planes) + off,
+                             min(65536u, a.plane_bytes - off), &bar);
+            for (uint32_t off = 0; off < a.slot_bytes; off += 65536u)
+                tma_bulk_g2s(reinterpret_cast<char*>(sslots) + off,
+                             reinterpret_cast<const char*>(a.slots) + off,
+                             min(65536u, a.slot_bytes - off), &bar);
+        }
+    }
+    mbar_wait(&bar, 0);
+    const uint32_t* planes = SMEM ? splanes : a.planes;
+    const uint32_t T_s = smem_u32(sdyn), R1_s = T_s + 4u * kSR1Off;
+    const uint32_t slots_s = smem_u32(sslots);
+    const uint32_t km[4] = {a.kmask[0], a.kmask[1], a.kmask[2], a.kmask[3]};
+    // this lane's real windows among its NWl (the rest are padding)
+    const int nvalid = min(a.NWl, max(0, a.W - (int)lane * a.NWl));
+    const uint32_t vmask = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
+    // r = 1 rounds: this lane applies update u of hit h of each round
+    const uint32_t uL = lane % NU, hL = lane / NU;
+    const uint32_t dword4 = r1_delta<X>(uL) * 4u;
+    const uint32_t r1row = R1_s + uL * 4u;
+    const bool r1lane = lane < (uint32_t)(HPR * NU);
+    const int l = LP + S;
+    unsigned long long scanned = 0, bscans = 0;
+
+    for (;;) {
+        unsigned long long bgrab = 0;
+        if (lane == 0) bgrab = atomicAdd(&a.st->next, (unsigned long long)a.batch);
+        bgrab = __shfl_sync(kFull, bgrab, 0);
+        if (bgrab >= a.span) break;
+        for (int sb = 0; sb < a.batch; sb += B::C) {
+            const unsigned long long cbase = a.lo_al + bgrab + sb;
+            if (cbase >= a.hi) break;
+            // the block's plane offsets: one row of base b_j per prefix position
+            uint32_t po[LP];  // byte offsets within a sequence's planes
+#pragma unroll
+            for (int j = 0; j < LP; ++j) {
+                const uint32_t bj = (uint32_t)(cbase >> (2 * (l - 1 - j))) & 3u;
+                po[j] = ((uint32_t)(j * 128) + bj * 32u + lane) * 4u;
+                asm volatile("" : "+r"(po[j]));  // keep in a register (no per-scan remat)
+            }
+            uint32_t alive[KW];
+#pragma unroll
+            for (int k = 0; k < KW; ++k) alive[k] = kFull;
+            if (cbase < a.lo || cbase + B::C > a.hi) {  // edge block of [lo, hi)
+#pragma unroll 1
+                for (int k = 0; k < KW; ++k) {
+                    uint32_t m = 0u;
+#pragma unroll 1
+                    for (uint32_t bb = 0; bb < 32; ++bb) {
+                        const unsigned long long c = cbase + blk_sfx<Bp32, S>(lane, k, bb);
+                        if (c >= a.lo && c < a.hi) m |= 1u << bb;
+                    }
+#pragma unroll
+                    for (int q = 0; q < KW; ++q)
+                        if (q == k) alive[q] = m;
+                }
+            }
+            int i = 0;
+            bool dead = false;
+            int nalive = B::C;
+            for (; i < a.n; ++i) {
+                if (i > 0 && a.skip && nalive <= a.handoff) break;
+                // ---- pass 1: class masks of this lane's windows
+                const char* P = reinterpret_cast<const char*>(planes) + (size_t)i * (LP * 512);
+                uint32_t m[LP];
+#pragma unroll
+                for (int j = 0; j < LP; ++j) {
+                    PMS_CHECK(po[j] < (uint32_t)(LP * 512));
+                    m[j] = *reinterpret_cast<const uint32_t*>(P + po[j]);
+                }
+                uint32_t c[5];
+                slice_count<LP>(m, km, c);
+                const uint32_t hv = c[4] & vmask;
+                const uint32_t up = c[1] | c[2] | c[3];
+                uint32_t r0m = hv & ~c[0] & ~up;
+                uint32_t r1m = hv & c[0] & ~up;
+                uint32_t r2m = hv & up;
+                // slot row of this lane's windows in sequence i
+                const uint32_t srow = (uint32_t)(i * a.Wp) + lane * (uint32_t)a.NWl;
+                auto slot_of = [&](int q) -> uint32_t {
+                    PMS_CHECK((int)lane * a.NWl + q < a.Wp);
+                    if constexpr (SMEM) return lds16(slots_s + 2u * (srow + (uint32_t)q));
+                    else return __ldg(a.slots + srow + (uint32_t)q);
+                };
+                uint32_t common = 0u;
+                const uint32_t n012 =
+                    (uint32_t)__popc(r0m) | ((uint32_t)__popc(r1m) << 10) | ((uint32_t)__popc(r2m) << 20);
+                const uint32_t tot = __reduce_add_sync(kFull, n012);
+                const uint32_t t0 = tot & 1023u, t1 = (tot >> 10) & 1023u, t2 = tot >> 20;
+                if (t0 <= (uint32_t)kSliceCap0 && t1 <= (uint32_t)kSliceCap1 &&
+                    t2 <= (uint32_t)kSliceCap2) {
+                    // ---- pass 2: queue the hits (one atomic claims all three
+                    // queue positions), then resolve them full-width
+                    if (n012) {
+                        const uint32_t pos = atom_add(qc_s, n012);
+                        uint32_t a0 = q0_s + 2u * (pos & 1023u);
+                        uint32_t a1 = q1_s + 2u * ((pos >> 10) & 1023u);
+                        uint32_t a2 = q2_s + 4u * (pos >> 20);
+                        while (r0m) {
+                            const int q = msb(r0m);
+                            r0m ^= 1u << q;
+                            sts16(a0, slot_of(q));
+                            a0 += 2u;
+                        }
+                        while (r1m) {
+                            const int q = msb(r1m);
+                            r1m ^= 1u << q;
+                            sts16(a1, slot_of(q));
+                            a1 += 2u;
+                        }
+                        while (r2m) {
+                            const int q = msb(r2m);
+                            r2m ^= 1u << q;
+                            sts32(a2, slot_of(q) | (slice_r(c, q) << 16));
+                            a2 += 4u;
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) sts32(qc_s, 0u);  // claims are done; next use after __syncwarp
+#pragma unroll 1
+                    for (uint32_t b0 = lane; b0 < t0; b0 += 32u) {
+                        const uint32_t sl = lds16(q0_s + 2u * b0);
+                        red_or(acc_s + (sl >> 5) * 4u, 1u << (sl & 31u));
+                    }
+#pragma unroll 1
+                    for (uint32_t b1 = hL; b1 < t1; b1 += HPR) {
+                        if (r1lane) {
+                            const uint32_t sl = lds16(q1_s + 2u * b1);
+                            red_or((acc_s + (sl >> 5) * 4u) ^ dword4, lds32(r1row + (sl & 31u) * 64u));
+                        }
+                    }
+#pragma unroll 1
+                    for (uint32_t b2 = 0; b2 < t2; ++b2) {
+                        const uint32_t e = lds32(q2_s + 4u * b2);  // same address: broadcast
+                        slice_bcast<X>(e & 0xFFFFu, e >> 16, lane, T_s, acc_s, common);
+                    }
+                } else {
+                    // dense hits (a queue would overflow): per-lane resolution
+                    while (r0m) {
+                        const int q = msb(r0m);
+                        r0m ^= 1u << q;
+                        const uint32_t sl = slot_of(q);
+                        red_or(acc_s + (sl >> 5) * 4u, 1u << (sl & 31u));
+                    }
+                    while (r1m) {
+                        const int q = msb(r1m);
+                        r1m ^= 1u << q;
+                        const uint32_t sl = slot_of(q);
+                        const uint32_t base = acc_s + (sl >> 5) * 4u;
+#pragma unroll
+                        for (int u = 0; u < NU; ++u)
+                            red_or(base ^ (r1_delta<X>((uint32_t)u) * 4u),
+                                   lds32(R1_s + ((sl & 31u) * 16u + (uint32_t)u) * 4u));
+                    }
+                    while (__any_sync(kFull, r2m != 0u)) {
+                        uint32_t rec = kFull;
+                        if (r2m) {
+                            const int q = msb(r2m);
+                            r2m ^= 1u << q;
+                            rec = slot_of(q) | (slice_r(c, q) << 16);
+                        }
+                        uint32_t who = __ballot_sync(kFull, rec != kFull);
+                        while (who) {
+                            const int src = msb(who);
+                            who ^= 1u << src;
+                            const uint32_t e = __shfl_sync(kFull, rec, src);
+                            slice_bcast<X>(e & 0xFFFFu, e >> 16, lane, T_s, acc_s, common);
+                        }
+                    }
+                }
+                // ---- end of scan: alive &= (the lane's words | common); clear them
+                __syncwarp();
+                int na = 0;
+#pragma unroll
+                for (int k = 0; k < KW; ++k) {
+                    const uint32_t wa = acc_s + (k * 32u + lane) * 4u;
+                    alive[k] &= lds32(wa) | common;
+                    sts32(wa, 0u);
+                    na += __popc(alive[k]);
+                }
+                __syncwarp();
+                ++bscans;
+                nalive = __reduce_add_sync(kFull, na);
+                if (nalive == 0) {  // skip rule for the whole block
+                    dead = true;
+                    if (a.skip) break;
+                }
+            }
+            if (dead) continue;
+            if (i == a.n) {  // every alive candidate matched all n sequences
+#pragma unroll
+                for (int k = 0; k < KW; ++k) {
+                    if (!alive[k]) continue;
+                    unsigned long long slot = atomicAdd(a.nout, (unsigned long long)__popc(alive[k]));
+                    for (uint32_t mm = alive[k]; mm; mm &= mm - 1, ++slot) {
+                        const unsigned long long code = cbase + blk_sfx<Bp32, S>(lane, k, __ffs(mm) - 1);
+                        if (slot < a.cap) {
+                            if (a.out_wide) static_cast<unsigned long long*>(a.out)[slot] = code;
+                            else static_cast<uint32_t*>(a.out)[slot] = (uint32_t)code;
+                        }
+                    }
+                }
+                continue;
+            }
+            // at most a.handoff survivors: the whole warp finishes each one from
+            // sequence i with the per-candidate check (packed words, L1/L2)
+            for (;;) {
+                uint32_t pick = kFull;
+#pragma unroll
+                for (int k = KW - 1; k >= 0; --k)
+                    if (alive[k]) pick = ((uint32_t)k << 5) | (__ffs(alive[k]) - 1);
+                const uint32_t holder = __ballot_sync(kFull, pick != kFull);
+                if (!holder) break;
+                const int src = __ffs(holder) - 1;
+                const uint32_t pk = __shfl_sync(kFull, pick, src);
+                const uint32_t k = pk >> 5;
+                if ((int)lane == src) {
+#pragma unroll
+                    for (int q = 0; q < KW; ++q)
+                        if (q == (int)k) alive[q] &= alive[q] - 1;
+                }
+                const unsigned long long code = cbase + blk_sfx<Bp32, S>(src, k, pk & 31u);
+                if (check_sequences<Bp32>(a.words, i, a.n, a.Wp, Bp32::prep(code), a.dp, (int)lane,
+                                          scanned)) {
+                    if (lane == 0) {
+                        const unsigned long long slot = atomicAdd(a.nout, 1ull);
+                        if (slot < a.cap) {
+                            if (a.out_wide) static_cast<unsigned long long*>(a.out)[slot] = code;
+                            else static_cast<uint32_t*>(a.out)[slot] = (uint32_t)code;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (lane == 0) {
+        if (scanned) atomicAdd(&a.st->extra, scanned);
+        if (bscans) atomicAdd(&a.st->block_scans, bscans);
+    }
+}
+
+}  // namespace

@@ -40,6 +40,19 @@ def _gpu():
 CAND = pms.Launch(algo=pms.ALGO_CANDIDATE)
 
 
+def auto_algo(t, l, d):
+    """The family PMS_ALGO_AUTO runs (include/pms.h): SLICE where it applies
+    (l <= 16, W <= 1024, 1 <= d + 1 <= l - S), else BLOCK for l >= 5, else
+    CANDIDATE."""
+    if l < 5:
+        return pms.ALGO_CANDIDATE
+    S = 6 if l >= 13 else 5
+    lp = l - S
+    if l <= 16 and t - l + 1 <= 1024 and lp >= 1 and d < lp:
+        return pms.ALGO_SLICE
+    return pms.ALGO_BLOCK
+
+
 def gpu(seqs, l, d, **kw):
     r = pms.find_ex(seqs, l, d, max_out=kw.pop("max_out", 1 << 22), **kw)
     return r
@@ -65,7 +78,7 @@ def test_tiny_random_instances(orc):
         d = rng.randint(0, min(3, l))
         s = fmgen.random_sequences(n, t, 500 + trial)
         got, _ = assert_same(s, l, d, orc)  # default family (AUTO)
-        assert got.stats.algo == (pms.ALGO_BLOCK if l >= 5 else pms.ALGO_CANDIDATE)
+        assert got.stats.algo == auto_algo(t, l, d)
         assert_same(s, l, d, orc, launch=CAND)
 
 
@@ -405,7 +418,8 @@ def test_block_algo_baseline_configs(orc, path):
     s, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
     for launch in BLOCKS + [None]:  # both block sizes and the default (AUTO) family
         r = gpu(s, g["l"], g["d"], launch=launch)
-        assert r.status == 0 and r.stats.algo == pms.ALGO_BLOCK
+        assert r.status == 0
+        assert r.stats.algo == (pms.ALGO_BLOCK if launch is not None else pms.ALGO_SLICE)
         assert r.count == g["count"] and r.codes.tolist() == g["codes"]
 
 
