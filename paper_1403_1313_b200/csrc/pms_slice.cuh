@@ -76,9 +76,6 @@ using SliceFn = void (*)(SliceArgs);
 // upper position away); 15: 0.
 constexpr int kSR1Off = 7 * 1024;
 constexpr int kSTWords = kSR1Off + 32 * 16;  // 30 KB
-constexpr int kSliceCap0 = 256;              // per-warp r = 0 queue entries (u16 slots)
-constexpr int kSliceCap1 = 128;              // per-warp r = 1 queue entries (u16 slots)
-constexpr int kSliceCap2 = 64;               // per-warp r >= 2 queue entries (slot | r << 16)
 constexpr int kSliceMaxLP = 11;              // l <= 16, S >= 5
 constexpr int kSlicePackThreads = 256;
 
@@ -90,8 +87,17 @@ struct SliceCfg {
     static constexpr int KW = 1 << (2 * X);   // mask words per lane
     static constexpr int NU = 6 + 3 * X;      // words of a radius-1 ball
     static constexpr int HPR = 32 / NU;       // r = 1 hits per round
-    static constexpr int NT = S >= 7 ? 512 : 1024;
+#ifndef PMS_SLICE7_NT
+#define PMS_SLICE7_NT 1024
+#endif
+    static constexpr int NT = S >= 7 ? PMS_SLICE7_NT : 1024;
     static constexpr int NWARP = NT / 32;
+    // per-warp queue capacities (a scan whose hits exceed one resolves them
+    // per lane instead): r = 0 / r = 1 entries are u16 slots, r >= 2 entries
+    // are slot | r << 16
+    static constexpr int kCap0 = S >= 7 ? 192 : 256;
+    static constexpr int kCap1 = S >= 7 ? 96 : 128;
+    static constexpr int kCap2 = S >= 7 ? 32 : 64;
     // dynamic shared memory in front of the staged tables: [ball table]
     // [per-warp candidate words][r = 0 / 1 queues][r >= 2 queues]; the word
     // blocks start at a multiple of their size (30 KB = 15 x 2 KB)
@@ -99,8 +105,8 @@ struct SliceCfg {
     static constexpr uint32_t kAccOff = kSTWords * 4u;     // (+ up to kAccAlign - 1 at run time)
     static constexpr uint32_t kAccBytes = NWARP * 32u * KW * 4u + kAccAlign;
     static constexpr uint32_t kQ01Off = kAccOff + kAccBytes;
-    static constexpr uint32_t kQ2Off = kQ01Off + NWARP * (kSliceCap0 + kSliceCap1) * 2u;
-    static constexpr uint32_t kWorkBytes = kQ2Off + NWARP * kSliceCap2 * 4u;  // = planes offset
+    static constexpr uint32_t kQ2Off = kQ01Off + NWARP * (kCap0 + kCap1) * 2u;
+    static constexpr uint32_t kWorkBytes = kQ2Off + NWARP * kCap2 * 4u;  // = planes offset
     static_assert(kWorkBytes % 128u == 0, "TMA destinations");
 };
 
@@ -316,9 +322,9 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
     // base alignment is not guaranteed beyond 128 B)
     const uint32_t acc0_s = (dyn_s + C::kAccOff + C::kAccAlign - 1u) & ~(C::kAccAlign - 1u);
     const uint32_t acc_s = acc0_s + wid * C::kAccAlign;
-    const uint32_t q0_s = dyn_s + C::kQ01Off + wid * ((kSliceCap0 + kSliceCap1) * 2u);
-    const uint32_t q1_s = q0_s + 2u * kSliceCap0;
-    const uint32_t q2_s = dyn_s + C::kQ2Off + wid * (kSliceCap2 * 4u);
+    const uint32_t q0_s = dyn_s + C::kQ01Off + wid * ((C::kCap0 + C::kCap1) * 2u);
+    const uint32_t q1_s = q0_s + 2u * C::kCap0;
+    const uint32_t q2_s = dyn_s + C::kQ2Off + wid * (C::kCap2 * 4u);
     const uint32_t qc_s = smem_u32(&qcnts[wid]);
     PMS_CHECK((acc_s & (32u * KW * 4u - 1u)) == 0u);
 #pragma unroll
@@ -423,8 +429,8 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
                     (uint32_t)__popc(r0m) | ((uint32_t)__popc(r1m) << 10) | ((uint32_t)__popc(r2m) << 20);
                 const uint32_t tot = __reduce_add_sync(kFull, n012);
                 const uint32_t t0 = tot & 1023u, t1 = (tot >> 10) & 1023u, t2 = tot >> 20;
-                if (t0 <= (uint32_t)kSliceCap0 && t1 <= (uint32_t)kSliceCap1 &&
-                    t2 <= (uint32_t)kSliceCap2) {
+                if (t0 <= (uint32_t)C::kCap0 && t1 <= (uint32_t)C::kCap1 &&
+                    t2 <= (uint32_t)C::kCap2) {
                     // ---- pass 2: queue the hits (one atomic claims all three
                     // queue positions), then resolve them full-width
                     if (n012) {

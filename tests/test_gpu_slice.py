@@ -62,22 +62,23 @@ def check(seqs, l, d, orc, lo=0, hi=None, launch=None, expect_slice=None):
 
 
 @pytest.mark.parametrize("path", GOLDEN_FILES, ids=[os.path.basename(p) for p in GOLDEN_FILES])
-@pytest.mark.parametrize("S", [0, 5, 6])
+@pytest.mark.parametrize("S", [0, 5, 6, 7])
 def test_slice_baseline_configs_against_golden(orc, path, S):
     g = json.load(open(path))
     s, rec = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
     assert rec.consensus == g["consensus"]
     r = pms.find_ex(s, g["l"], g["d"], launch=slice_launch(S), max_out=1 << 22)
     assert r.status == 0
-    assert r.stats.algo == pms.ALGO_SLICE
+    S_ran = S or (7 if g["l"] >= 14 else 6 if g["l"] >= 13 else 5)
+    assert (r.stats.algo == pms.ALGO_SLICE) == applies(g["t"], g["l"], g["d"], S_ran)
     assert r.count == g["count"] and r.codes.tolist() == g["codes"]
 
 
-@pytest.mark.parametrize("S", [5, 6])
+@pytest.mark.parametrize("S", [5, 6, 7])
 def test_slice_tiny_random(orc, S):
     rng = random.Random(5150 + S)
     for trial in range(120):
-        l = rng.randint(S + 1, 12)
+        l = rng.randint(S + 1, max(12, S + 4))
         n = rng.randint(1, 6)
         t = rng.randint(l, 140)
         d = rng.randint(0, min(6, l - S - 1))
@@ -93,7 +94,7 @@ def test_slice_planted_small(orc):
         assert code in set(got.codes.tolist())
 
 
-@pytest.mark.parametrize("S", [5, 6])
+@pytest.mark.parametrize("S", [5, 6, 7])
 def test_slice_ranges_and_additivity(orc, S):
     L = slice_launch(S)
     s, _ = fmgen.generate_fm(5, 60, 9, 2, 4)
@@ -137,7 +138,7 @@ def test_slice_dense_hits_queue_overflow(orc):
 def test_slice_l16_and_prefix_lengths(orc):
     # every prefix length LP = l - S of both block sizes, d from 0 to LP - 1
     rng = random.Random(99)
-    for S in (5, 6):
+    for S in (5, 6, 7):
         for l in range(S + 1, 17):
             d = rng.randint(0, l - S - 1)
             s = fmgen.random_sequences(3, 60, 1000 * S + l)
@@ -150,9 +151,10 @@ def test_slice_ineligible_d_and_auto(orc):
     """d >= l - S (every window a hit) runs the block family; AUTO picks the
     slice family exactly where it applies."""
     for (n, t, l, d) in [(3, 40, 7, 2), (3, 40, 7, 1), (4, 60, 9, 4), (4, 60, 9, 3),
-                         (2, 30, 13, 7), (2, 30, 13, 6), (5, 80, 11, 2)]:
+                         (2, 30, 13, 7), (2, 30, 13, 6), (5, 80, 11, 2), (2, 30, 14, 6),
+                         (2, 30, 14, 7), (3, 40, 15, 4)]:
         s = fmgen.random_sequences(n, t, l * 10 + d)
-        S = 6 if l >= 13 else 5
+        S = 7 if l >= 14 else 6 if l >= 13 else 5
         check(s, l, d, orc, expect_slice=applies(t, l, d, S))
 
 
@@ -161,7 +163,7 @@ def test_slice_no_skip_and_handoff(orc):
     want = orc.find(s, 10, 2).codes.tolist()
     for kw in [dict(no_skip=1), dict(handoff=0), dict(handoff=1), dict(handoff=5),
                dict(handoff=60), dict(handoff=5000)]:
-        for S in (5, 6):
+        for S in (5, 6, 7):
             r = pms.find_ex(s, 10, 2, launch=slice_launch(S, **kw))
             assert r.status == 0 and r.stats.algo == pms.ALGO_SLICE
             assert r.codes.tolist() == want, (S, kw)
@@ -172,7 +174,7 @@ def test_slice_no_skip_and_handoff(orc):
 def test_slice_launch_invariance_and_global_tables(orc):
     s, _ = fmgen.generate_fm(20, 600, 11, 3, 1)
     base = orc.find(s, 11, 3).codes.tolist()
-    for S in (5, 6):
+    for S in (5, 6, 7):
         for kw in [dict(), dict(grid_ctas=1), dict(grid_ctas=5), dict(batch=4096),
                    dict(batch=12288), dict(table_global=1)]:
             r = pms.find_ex(s, 11, 3, launch=slice_launch(S, **kw))
