@@ -49,7 +49,13 @@ enum {
                              entry points), l>t, d<0, lo>hi,
                              uint32 output from a plan with l>16 */
     PMS_E_CHAR = -2,      /* a byte outside "ACGTacgt" (incl. 'N') */
-    PMS_E_TOO_LARGE = -3, /* n*t or the packed table exceeds 2^31 bytes */
+    PMS_E_TOO_LARGE = -3, /* n*t or the packed table exceeds 2^31 bytes.
+                             (SURVEY 8(b) reserved this status for a window
+                             table larger than shared memory; here such a
+                             table is read through L1/L2 instead -- the same
+                             result, pms_stats.table_in_smem = 0 -- so the
+                             status only marks sizes the 32-bit indexing
+                             cannot address.)                              */
     PMS_E_CUDA = -4,      /* no device, allocation/launch/runtime failure */
     PMS_E_TRUNCATED = -5  /* more motifs than max_out; *count is exact */
 };
@@ -239,6 +245,25 @@ void pms_plan_destroy(pms_plan *plan);
 int pms_roofline(int32_t iters, double *compares_per_s,
                  double *compares_per_clk_sm, double *ms);
 
+/* ---------------------------------------------------------------------
+ * Roofline microbenchmark of the slice family:
+ * runs the plan's own per-scan code on the tables of its last execution
+ * (pms_plan_execute*, completed or not: this call waits for it) with
+ * everything dynamic removed -- no work counter, no skip rule, no hand-off,
+ * no output; warp g scans block (g + k * warps) mod 4^(l-S) against sequence
+ * (g + k) mod n for k < scans_per_warp, every warp busy throughout.
+ *   mode 0: pass 1 only (plane loads + carry-save hit classification): R_pass1
+ *   mode 1: pass 1 + hit resolution + end of scan at the instance's own hit
+ *           mix: R_scan
+ *   tests_per_s  receives (block, sequence) scans * W / second (required)
+ *   scans_per_s, ms  scans / second and the kernel time (may be NULL)
+ * PMS_E_ARG unless the plan runs PMS_ALGO_SLICE with its tables in shared
+ * memory and has been executed; CUDA-event timed, best of three after one
+ * warm-up, on the plan's private stream.
+ * ------------------------------------------------------------------- */
+int pms_plan_roofline(pms_plan *plan, int32_t mode, int32_t scans_per_warp,
+                      double *tests_per_s, double *scans_per_s, double *ms);
+
 /* Static description of a status code. */
 const char *pms_strerror(int status);
 
@@ -246,9 +271,11 @@ const char *pms_strerror(int status);
  * line and CUDA error string); "" if none.  Owned by the library. */
 const char *pms_last_error(void);
 
-/* Debug builds (libpms_b200_debug.so, -DPMS_DEBUG_CHECKS) count out-of-range
- * device indices instead of accessing them; returns the count (reset to 0 if
- * `reset`), -1 in release builds, -2 on a device error. */
+/* Debug builds (libpms_b200_debug.so, -DPMS_DEBUG_CHECKS) count failed
+ * device checks -- out-of-range indices and hit-queue / candidate-word protocol
+ * violations; the checked access itself still runs, the count
+ * is a detector.  Returns the count (reset to 0 if `reset`), -1 in release
+ * builds, -2 on a device error. */
 int64_t pms_debug_violations(int32_t reset);
 
 /* Number of SMs and the opt-in shared memory per block of the current

@@ -99,6 +99,10 @@ def load() -> ctypes.CDLL:
                                      ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_double)]
         lib.pms_roofline.restype = ctypes.c_int
+        lib.pms_plan_roofline.argtypes = [vp, i32, i32, ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_double)]
+        lib.pms_plan_roofline.restype = ctypes.c_int
         lib.pms_strerror.argtypes = [ctypes.c_int]
         lib.pms_strerror.restype = ctypes.c_char_p
         lib.pms_debug_violations.argtypes = [ctypes.c_int32]
@@ -257,6 +261,17 @@ class Plan:
         assert out.is_cuda and out.element_size() in (4, 8)
         self.execute(seqs.data_ptr(), lo, hi, out.data_ptr() if out.numel() else 0, out.numel(),
                      count.data_ptr(), stream.cuda_stream, wide=wide)
+
+    def roofline(self, mode: int, scans_per_warp: int = 64) -> dict:
+        """pms_plan_roofline: the plan's per-scan code without its dynamic
+        parts (mode 0: pass 1 only, R_pass1; mode 1: the whole scan, R_scan)
+        on the tables of its last execution."""
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        s = self._lib.pms_plan_roofline(self._h, int(mode), int(scans_per_warp), ctypes.byref(a),
+                                        ctypes.byref(b), ctypes.byref(c))
+        if s != OK:
+            raise PmsError(s, "pms_plan_roofline")
+        return dict(tests_per_s=a.value, scans_per_s=b.value, ms=c.value)
 
     def wait(self) -> tuple[int, Stats]:
         st = Stats()

@@ -13,10 +13,12 @@ LIB_DEBUG = os.path.join(PKG, "libpms_b200_debug.so")  # -DPMS_DEBUG_CHECKS (bou
 LIB = LIB_DEBUG if os.environ.get("PMS_DEBUG_LIB") == "1" else LIB_RELEASE
 # PMS_LIB_OVERRIDE=/path/lib.so loads a variant build (tuning experiments, scripts/variants.py)
 LIB = os.environ.get("PMS_LIB_OVERRIDE") or LIB
-# pms.cu: 32-bit-word kernels + host code; pms64.cu: 64-bit-word kernels (l <= 31)
-SOURCES = [os.path.join(CSRC, "pms.cu"), os.path.join(CSRC, "pms64.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "pms_device.cuh"), os.path.join(CSRC, "pms_kernels.cuh"),
-                  os.path.join(ROOT, "include", "pms.h")]
+# pms.cu: 32-bit-word kernels + host code; pms64.cu: 64-bit-word kernels (l <= 31);
+# pms_slice.cu / pms_roof.cu: the slice family's kernels and roofline kernels
+SOURCES = [os.path.join(CSRC, f) for f in ("pms.cu", "pms64.cu", "pms_slice.cu", "pms_roof.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, h) for h in ("pms_device.cuh", "pms_kernels.cuh",
+                                                    "pms_slice.cuh")] + \
+    [os.path.join(ROOT, "include", "pms.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-O3"]

@@ -145,24 +145,13 @@ const BlockKernel kBlockKernels[] = {
     {6, 0, pms_search_block<Bp32, 6, true, 0>, pms_search_block<Bp32, 6, false, 0>},
     PMS_NWB_LIST(PMS_BLK5) PMS_NWB_LIST(PMS_BLK6)};
 
-// PMS_ALGO_SLICE instances: block digits S x prefix length LP = l - S
-// (l <= 16), table staged in shared memory or read through L1/L2
-struct SliceKernel {
-    int S, LP;
-    SliceFn fn_smem, fn_global;
-};
-#define PMS_SLICE(S, LP) {S, LP, pms_search_slice<S, LP, true>, pms_search_slice<S, LP, false>},
-#define PMS_SLICE5(LP) PMS_SLICE(5, LP)
-#define PMS_SLICE6(LP) PMS_SLICE(6, LP)
-#define PMS_SLICE7(LP) PMS_SLICE(7, LP)
-#define PMS_LP_LIST(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9)
-const SliceKernel kSliceKernels[] = {PMS_LP_LIST(PMS_SLICE5) PMS_SLICE5(10) PMS_SLICE5(11)
-                                     PMS_LP_LIST(PMS_SLICE6) PMS_SLICE6(10)
-                                     PMS_LP_LIST(PMS_SLICE7)};
-
+// PMS_ALGO_SLICE instances (pms_slice.cu) and their roofline kernels
+// (pms_roof.cu): block digits S x prefix length LP = l - S
 const SliceKernel* find_slice_kernel(int S, int LP) {
-    for (const SliceKernel& k : kSliceKernels)
-        if (k.S == S && k.LP == LP) return &k;
+    int cnt = 0;
+    const SliceKernel* ks = slice_kernels(&cnt);
+    for (int q = 0; q < cnt; ++q)
+        if (ks[q].S == S && ks[q].LP == LP) return &ks[q];
     return nullptr;
 }
 
@@ -251,7 +240,8 @@ const uint32_t* ensure_ball_table(int dev) {
             for (int j = 0; j < 6; ++j) h[kR1Off + e * 8 + j] = h[1024 + e * 32 + kM[j]];
         uint32_t* d = nullptr;
         if (cudaMalloc(&d, kTWords * 4) != cudaSuccess) return nullptr;
-        if (cudaMemcpy(d, h.data(), kTWords * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        if (cudaMemcpy(d, h.data(), kTWords * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {
             cudaFree(d);
             return nullptr;
         }
@@ -302,7 +292,9 @@ int ensure_constants() {
     if (dev_done[dev]) return PMS_OK;
     uint32_t h[kSub];
     for (int i = 0; i < kSub; ++i) h[i] = code_to_bp((uint32_t)i);
-    if (cudaMemcpyToSymbol(c_bp256, h, sizeof(h)) != cudaSuccess) return fail_cuda(__LINE__);
+    if (cudaMemcpyToSymbol(c_bp256, h, sizeof(h)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
+        return fail_cuda(__LINE__);
     dev_done[dev] = 1;
     return PMS_OK;
 }
@@ -582,7 +574,11 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     if (cudaMalloc(&p->d_table, p->tab_bytes) != cudaSuccess ||
         cudaMalloc(&p->d_state, sizeof(DevState)) != cudaSuccess ||
         cudaMallocHost(&p->h_state, sizeof(DevState)) != cudaSuccess ||
-        cudaMemset(p->d_state, 0, sizeof(DevState)) != cudaSuccess) {
+        cudaMemset(p->d_state, 0, sizeof(DevState)) != cudaSuccess ||
+        // one-time setup above ran on the legacy stream (cudaMemset, the ball
+        // table and constant copies); the work streams are non-blocking, so
+        // wait for it here rather than rely on stream ordering
+        cudaDeviceSynchronize() != cudaSuccess) {
         destroy_plan(p);
         return fail_cuda(__LINE__);
     }
@@ -602,6 +598,24 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
 extern "C" void pms_plan_destroy(pms_plan* plan) { destroy_plan(plan); }
 
 namespace {
+
+// The slice kernels' arguments that depend on the plan only (tables, shape,
+// threshold masks, skip rule and hand-off).
+SliceArgs slice_args(const pms_plan* p) {
+    SliceArgs sa{};
+    sa.planes = static_cast<const uint32_t*>(p->d_planes);
+    sa.slots = static_cast<const uint16_t*>(p->d_slots);
+    sa.words = static_cast<const uint32_t*>(p->d_table);
+    sa.ball = p->d_ball;
+    sa.n = p->n; sa.W = p->W; sa.Wp = p->Wp; sa.NWl = p->NWl;
+    sa.dp = (uint32_t)std::min(p->d, p->l);
+    const uint32_t K = 16u - (uint32_t)(p->LP - p->d);  // 1 <= LP - d <= LP
+    for (int b = 0; b < 4; ++b) sa.kmask[b] = ((K >> b) & 1u) ? 0xFFFFFFFFu : 0u;
+    sa.skip = p->launch.no_skip ? 0 : 1;
+    sa.handoff = p->launch.handoff > 0 ? p->launch.handoff : (p->d >= 5 ? 2 : 1);
+    sa.plane_bytes = p->plane_bytes; sa.slot_bytes = p->slot_bytes;
+    return sa;
+}
 
 // out_wide: d_out holds uint64 codes (pms_plan_execute64) instead of uint32
 // timed = false (pms_find* without stats): no event between the pre-pass and
@@ -650,26 +664,17 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     a.epoch = p->epoch;
     static const bool no_pdl = std::getenv("PMS_NO_PDL") != nullptr;
     if (p->algo == PMS_ALGO_SLICE) {
-        SliceArgs sa{};
-        sa.planes = static_cast<const uint32_t*>(p->d_planes);
-        sa.slots = static_cast<const uint16_t*>(p->d_slots);
-        sa.words = static_cast<const uint32_t*>(p->d_table);
-        sa.ball = p->d_ball;
-        sa.n = p->n; sa.W = p->W; sa.Wp = p->Wp; sa.NWl = p->NWl;
-        sa.dp = (uint32_t)std::min(p->d, p->l);
-        const uint32_t K = 16u - (uint32_t)(p->LP - p->d);  // 1 <= LP - d <= LP
-        for (int b = 0; b < 4; ++b) sa.kmask[b] = ((K >> b) & 1u) ? 0xFFFFFFFFu : 0u;
+        SliceArgs sa = slice_args(p);
         sa.lo = lo; sa.hi = hi; sa.lo_al = lo_al; sa.span = span; sa.batch = batch;
-        sa.skip = p->launch.no_skip ? 0 : 1;
-        sa.handoff = p->launch.handoff > 0 ? p->launch.handoff : (p->d >= 5 ? 2 : 1);
         sa.out_wide = out_wide;
-        sa.plane_bytes = p->plane_bytes; sa.slot_bytes = p->slot_bytes;
         sa.st = p->d_state; sa.epoch = p->epoch;
         sa.nout = reinterpret_cast<unsigned long long*>(d_count);
         sa.out = d_out; sa.cap = cap;
         if (cudaEventRecord(p->ev[0], s) != cudaSuccess) return fail_cuda(__LINE__);
-        auto pack = p->S == 5 ? pms_pack_slice<5> : p->S == 6 ? pms_pack_slice<6> : pms_pack_slice<7>;
-        pack<<<(unsigned)p->n, kSlicePackThreads, 0, s>>>(
+        const SlicePackFn pack = slice_pack_kernel(p->S);
+        const unsigned pack_y =
+            (unsigned)((p->Wp + p->LP * 128 + kSlicePackThreads - 1) / kSlicePackThreads);
+        pack<<<dim3((unsigned)p->n, pack_y), kSlicePackThreads, 0, s>>>(
             d_seqs, p->n, p->t, p->l, p->W, p->NWl, p->LP, static_cast<uint32_t*>(p->d_planes),
             static_cast<uint16_t*>(p->d_slots), static_cast<uint32_t*>(p->d_table), p->d_state,
             reinterpret_cast<unsigned long long*>(d_count), p->epoch);
@@ -856,7 +861,8 @@ int ctx_grow(CallCtx* c, unsigned long long bytes) {
     c->d_count = nullptr;
     c->out_bytes = 0;
     if (cudaMalloc(&c->d_buf, CallCtx::kHead + bytes) != cudaSuccess ||
-        cudaMemset(c->d_buf, 0, CallCtx::kHead) != cudaSuccess)
+        cudaMemset(c->d_buf, 0, CallCtx::kHead) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)  // (legacy-stream memset vs the context's stream)
         return fail_cuda(__LINE__);
     c->d_out = c->d_buf + CallCtx::kHead;
     c->d_count = reinterpret_cast<uint64_t*>(c->d_buf + 64);
@@ -1156,6 +1162,55 @@ extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compa
     return PMS_OK;
 }
 
+extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_warp,
+                                 double* tests_per_s, double* scans_per_s, double* ms) {
+    if (!p || !tests_per_s || p->algo != PMS_ALGO_SLICE || !p->in_smem || !p->executed ||
+        mode < 0 || mode > 1 || scans_per_warp < 1)
+        return PMS_E_ARG;
+    const SliceRoofFn fn = slice_roofline_kernel(p->S, p->LP, mode);
+    if (!fn) return PMS_E_ARG;
+    // the tables of the plan's last execution (its pre-pass) must be complete
+    if (cudaEventSynchronize(p->ev[2]) != cudaSuccess) return fail_cuda(__LINE__);
+    int smem_optin = 0;
+    cudaFuncAttributes fa{};
+    if (cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->dev) !=
+            cudaSuccess ||
+        cudaFuncGetAttributes(&fa, (const void*)fn) != cudaSuccess ||
+        cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem_optin - (int)fa.sharedSizeBytes) != cudaSuccess)
+        return fail_cuda(__LINE__);
+    SliceArgs sa = slice_args(p);
+    unsigned long long* sink = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaMalloc(&sink, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+        cudaFree(sink);
+        return fail_cuda(__LINE__);
+    }
+    const unsigned long long nblocks = 1ull << (2 * p->LP);
+    cudaStream_t s = p->aux;
+    float best = 1e30f;
+    for (int r = 0; r < 4; ++r) {  // one warm-up, best of three
+        cudaEventRecord(e0, s);
+        fn<<<p->grid, p->block, p->smem_bytes, s>>>(sa, r == 0 ? 1 : scans_per_warp, nblocks, sink);
+        cudaEventRecord(e1, s);
+        if (cudaEventSynchronize(e1) != cudaSuccess) break;
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, e1);
+        if (r > 0) best = std::min(best, t);
+    }
+    const cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (err != cudaSuccess) return fail_cuda(__LINE__, err);
+    const double scans = (double)p->grid * (p->block / 32) * scans_per_warp;
+    *tests_per_s = scans * p->W / (best * 1e-3);
+    if (scans_per_s) *scans_per_s = scans / (best * 1e-3);
+    if (ms) *ms = best;
+    return PMS_OK;
+}
+
 extern "C" const char* pms_last_error(void) { return g_last_error; }
 
 extern "C" int64_t pms_debug_violations(int32_t reset) {
@@ -1167,9 +1222,13 @@ extern "C" int64_t pms_debug_violations(int32_t reset) {
         const unsigned int z = 0;
         cudaMemcpyToSymbol(pms::g_pms_violations, &z, sizeof(z));
     }
-    const int64_t v64 = pms::debug_violations64(reset);  // pms64.cu's own counter
-    if (v64 < 0) return v64;
-    return (int64_t)v + v64;
+    int64_t total = (int64_t)v;
+    for (int64_t x : {pms::debug_violations64(reset), pms::debug_violations_slice(reset),
+                      pms::debug_violations_roof(reset)}) {  // the other TUs' counters
+        if (x < 0) return x;
+        total += x;
+    }
+    return total;
 #else
     (void)reset;
     return -1;

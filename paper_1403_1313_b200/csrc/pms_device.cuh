@@ -18,10 +18,11 @@
 
 namespace pms {
 
-// Debug builds (-DPMS_DEBUG_CHECKS, libpms_b200_debug.so) count every
-// out-of-range index instead of performing the access's check silently; the
-// host reads the counter with pms_debug_violations().  No trap, so a bad index
-// cannot fault the device.  Release builds compile the checks away.
+// Debug builds (-DPMS_DEBUG_CHECKS, libpms_b200_debug.so) count every failed
+// check (out-of-range index, protocol violation) in a device counter the host
+// reads with pms_debug_violations().  A check is a detector, not a guard: the
+// access it precedes still runs (a bad index can still fault), but the count
+// makes a silent slip visible.  Release builds compile the checks away.
 #ifdef PMS_DEBUG_CHECKS
 static __device__ unsigned int g_pms_violations;  // one per translation unit
 #define PMS_CHECK(cond)                                          \

@@ -26,7 +26,8 @@ def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def gather_codes(local: np.ndarray, device=None, group=None) -> np.ndarray:
-    """All-gather variable-length uint32 code arrays; concatenated in rank order."""
+    """All-gather variable-length code arrays (uint64 end to end: l <= 31
+    codes need 62 bits); concatenated in rank order."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -36,12 +37,12 @@ def gather_codes(local: np.ndarray, device=None, group=None) -> np.ndarray:
     dist.all_gather(sizes, n, group=group)
     sizes = [int(s.item()) for s in sizes]
     cap = max(max(sizes), 1)
-    buf = torch.zeros(cap, dtype=torch.int64, device=dev)
+    buf = torch.zeros(cap, dtype=torch.int64, device=dev)  # codes < 2^62 fit int64
     if local.size:
         buf[:local.size] = torch.from_numpy(local.astype(np.int64)).to(dev)
     parts = [torch.zeros(cap, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(parts, buf, group=group)
-    return np.concatenate([p[:s].cpu().numpy() for p, s in zip(parts, sizes)]).astype(np.uint32)
+    return np.concatenate([p[:s].cpu().numpy() for p, s in zip(parts, sizes)]).astype(np.uint64)
 
 
 def max_over_ranks(x: float, device=None, group=None) -> float:
@@ -57,16 +58,18 @@ def max_over_ranks(x: float, device=None, group=None) -> float:
 def find_sharded(seqs, l: int, d: int, group=None,
                  search: Callable | None = None) -> np.ndarray:
     """Every rank searches its shard of [0, 4^l) and all ranks return the full
-    ascending motif set.  `search(seqs, l, d, lo, hi) -> codes` defaults to the
-    CUDA path on this rank's current device (pms.find)."""
+    ascending motif set (uint64 codes).  `search(seqs, l, d, lo, hi) -> codes`
+    defaults to the CUDA path on this rank's current device: pms.find (uint32
+    codes) for l <= 16, pms.find64 for 17 <= l <= 31."""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     lo, hi = shard_range(4 ** l, rank, world)
     if search is None:
-        from . import find
-        search = lambda s, l_, d_, a, b: find(s, l_, d_, lo=a, hi=b)  # noqa: E731
-    local = np.asarray(search(seqs, l, d, lo, hi), dtype=np.uint32)
+        from . import MAX_L, find, find64
+        f = find if l <= MAX_L else find64
+        search = lambda s, l_, d_, a, b: f(s, l_, d_, lo=a, hi=b)  # noqa: E731
+    local = np.asarray(search(seqs, l, d, lo, hi)).astype(np.uint64)
     dev = None
     if dist.get_backend(group) == "nccl":
         dev = torch.device("cuda", torch.cuda.current_device())

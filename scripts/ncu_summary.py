@@ -4,6 +4,7 @@ files back):
 
     python scripts/ncu_summary.py full REPORT.ncu-rep [--title ...]   # --set full capture
     python scripts/ncu_summary.py launches LAUNCHES.csv                 # gpu__time_duration list
+    python scripts/ncu_summary.py json REPORT.ncu-rep --scans N --out F  # bench.py's issue roofline
 
 `full` prints the pipe utilisations, issue rate, stall reasons and DRAM
 traffic of the captured kernel; `launches` groups the launch list by kernel
@@ -15,6 +16,7 @@ from __future__ import annotations
 import collections
 import csv
 import io
+import os
 import subprocess
 import sys
 
@@ -56,6 +58,42 @@ def full(rep: str, title: str) -> None:
         print()
 
 
+def to_json(rep: str, scans: int, out: str, kernel_note: str) -> None:
+    """The numbers bench.py's roofline object reads (profiles/slice_kernel_ncu.json):
+    warp instructions per block scan (smsp__inst_executed.sum / the launch's
+    block scans, from the same bench command's stats) and DRAM bytes per launch."""
+    import json
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, vals = rows[0], rows[2]
+
+    units = rows[1]
+
+    def num(k):
+        i = hdr.index(k)
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[i], 1.0)
+        return float(vals[i].replace(",", "")) * scale
+    inst = num("smsp__inst_executed.sum")
+    doc = {"kernel": vals[hdr.index("Kernel Name")], "note": kernel_note,
+           "source": os.path.relpath(rep) + " (ncu --set full --clock-control none)",
+           "warp_instructions_per_launch": inst, "block_scans_per_launch": scans,
+           "warp_instructions_per_scan": inst / scans,
+           "dram_bytes_per_launch": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
+           "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+           "ipc_per_sm": num("sm__inst_executed.avg.per_cycle_active"),
+           "alu_pipe_pct": num("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+           "lsu_pipe_pct": num("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+           "xu_pipe_pct": num("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+           "kernel_us": num("gpu__time_duration.sum") / (1e3 if "nsecond" in units[hdr.index(
+               "gpu__time_duration.sum")] else 1.0),
+           "shared_bank_conflicts": num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")}
+    with open(out, "w") as f:
+        json.dump(doc, f, indent=1)
+        f.write("\n")
+    print(json.dumps(doc, indent=1))
+
+
 def launches(path: str) -> None:
     lines = [ln for ln in open(path) if ln.startswith('"')]
     rows = list(csv.DictReader(io.StringIO("".join(lines))))
@@ -82,5 +120,9 @@ if __name__ == "__main__":
         full(sys.argv[2], title)
     elif len(sys.argv) >= 3 and sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif len(sys.argv) >= 3 and sys.argv[1] == "json":
+        a = sys.argv
+        to_json(a[2], int(a[a.index("--scans") + 1]), a[a.index("--out") + 1],
+                a[a.index("--note") + 1] if "--note" in a else "")
     else:
         raise SystemExit(__doc__)

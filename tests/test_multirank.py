@@ -71,3 +71,59 @@ def test_gloo_world2_sharded_search_and_gather(orc):
     for rank, got, t in res:
         assert got == want
         assert t == 2.0
+
+
+def _gpu_worker(rank: int, world: int, port: int, q, cases):
+    """One rank of a gloo group on cuda:0: find_sharded with its default
+    search, i.e. the CUDA path (pms.find / pms.find64) on this rank's shard."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1403_1313_b200.shard import find_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for (n, t, l, d, seed) in cases:
+            s, _ = fmgen.generate_fm(n, t, l, d, seed)
+            out.append(find_sharded(s, l, d).tolist())
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_cuda_path_against_golden(orc, world):
+    """the candidate range split over ranks (PAPER.md:75's
+    contiguous partition), each rank's shard searched by the CUDA kernels, one
+    gather; the union equals the oracle's golden set (bj2 = (13,3), bj3 =
+    (15,4), seed 1) and an l = 17 case exercises the 64-bit path.  All ranks
+    share cuda:0 (one GPU on this pool); their kernels never wait on each
+    other, so this is a correctness test of the sharded path, not a timing."""
+    import json
+    gold = [json.load(open(os.path.join(os.path.dirname(__file__), "golden", f)))
+            for f in ("bj2_seed1.json", "bj3_seed1.json")]
+    cases = [(g["n"], g["t"], g["l"], g["d"], g["seed"]) for g in gold] + [(6, 60, 17, 4, 3)]
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, cases)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    s17, rec = fmgen.generate_fm(6, 60, 17, 4, 3)
+    cons = int("".join(str("ACGT".index(c)) for c in rec.consensus), 4)
+    for _, got in res:
+        assert got[0] == gold[0]["codes"] and got[1] == gold[1]["codes"]
+        assert cons in got[2]
+        for c in got[2][:50]:
+            assert orc.verify_motif(s17, 17, 4, c)
+        # range additivity: the shard union over a window around the plant
+        near = orc.find64(s17, 17, 4, lo=max(0, cons - 50000), hi=cons + 50000).codes.tolist()
+        assert [c for c in got[2] if cons - 50000 <= c < cons + 50000] == near
