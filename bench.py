@@ -240,6 +240,11 @@ def roofline_object(pms, plan, st, search_ms: float, clk: dict, sms: int) -> dic
                r_pass1_basis="measured: pms_plan_roofline mode 0 -- the bit-sliced prefix "
                              "test alone (one-hot plane loads + carry-save classification)")
     ctx = ncu_context()
+    cfg = (ctx or {}).get("config") or {}
+    same = (cfg.get("n"), cfg.get("t"), cfg.get("l"), cfg.get("d"), cfg.get("block_digits")) == \
+        (plan.n, plan.t, plan.l, plan.d, st.block_digits)
+    if not same:  # the capture is of another workload: no per-launch numbers from it
+        ctx = None
     obj["traffic"] = ctx.get("dram_bytes_per_launch") if ctx else None
     if ctx and ctx.get("warp_instructions_per_scan") and clk.get("sm_mhz"):
         instr = ctx["warp_instructions_per_scan"] * st.block_scans

@@ -257,9 +257,10 @@ int pms_roofline(int32_t iters, double *compares_per_s,
  *           mix: R_scan
  *   tests_per_s  receives (block, sequence) scans * W / second (required)
  *   scans_per_s, ms  scans / second and the kernel time (may be NULL)
- * PMS_E_ARG unless the plan runs PMS_ALGO_SLICE with its tables in shared
- * memory and has been executed; CUDA-event timed, best of three after one
- * warm-up, on the plan's private stream.
+ * The tables are placed as the plan's search kernel places them (shared
+ * memory, or L1/L2 when they do not fit).  PMS_E_ARG unless the plan runs
+ * PMS_ALGO_SLICE and has been executed; CUDA-event timed, best of three
+ * after one warm-up, on the plan's private stream.
  * ------------------------------------------------------------------- */
 int pms_plan_roofline(pms_plan *plan, int32_t mode, int32_t scans_per_warp,
                       double *tests_per_s, double *scans_per_s, double *ms);

@@ -1164,10 +1164,10 @@ extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compa
 
 extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_warp,
                                  double* tests_per_s, double* scans_per_s, double* ms) {
-    if (!p || !tests_per_s || p->algo != PMS_ALGO_SLICE || !p->in_smem || !p->executed ||
-        mode < 0 || mode > 1 || scans_per_warp < 1)
+    if (!p || !tests_per_s || p->algo != PMS_ALGO_SLICE || !p->executed || mode < 0 ||
+        mode > 1 || scans_per_warp < 1)
         return PMS_E_ARG;
-    const SliceRoofFn fn = slice_roofline_kernel(p->S, p->LP, mode);
+    const SliceRoofFn fn = slice_roofline_kernel(p->S, p->LP, mode, p->in_smem != 0);
     if (!fn) return PMS_E_ARG;
     // the tables of the plan's last execution (its pre-pass) must be complete
     if (cudaEventSynchronize(p->ev[2]) != cudaSuccess) return fail_cuda(__LINE__);

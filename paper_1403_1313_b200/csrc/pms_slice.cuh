@@ -81,7 +81,7 @@ struct SliceKernel {
 };
 const SliceKernel* slice_kernels(int* count);              // pms_slice.cu
 SlicePackFn slice_pack_kernel(int S);                      // pms_slice.cu
-SliceRoofFn slice_roofline_kernel(int S, int LP, int mode);  // pms_roof.cu (staged tables)
+SliceRoofFn slice_roofline_kernel(int S, int LP, int mode, bool smem);  // pms_roof.cu
 int64_t debug_violations_slice(int reset);
 int64_t debug_violations_roof(int reset);
 
@@ -92,6 +92,12 @@ int64_t debug_violations_roof(int reset);
 constexpr int kSR1Off = 7 * 1024;
 constexpr int kSTWords = kSR1Off + 32 * 16;  // 30 KB
 constexpr int kSliceMaxLP = 11;              // l <= 16, S >= 5
+#ifndef PMS_SLICE_R0_DIRECT
+#define PMS_SLICE_R0_DIRECT 1  // r = 0 hits resolved per lane (no queue); 0: queued
+#endif
+#ifndef PMS_SLICE_R1_DIRECT
+#define PMS_SLICE_R1_DIRECT 0  // r = 1 hits resolved per lane (NU reds each); 0: queued
+#endif
 constexpr uint32_t kPoison16 = 0xFFFFu;      // debug builds: consumed / unwritten queue entry
 constexpr uint32_t kPoison32 = 0xFFFFFFFFu;  // (no real entry: slots < 2^14, r < 16)
 constexpr int kSlicePackThreads = 256;
@@ -333,6 +339,7 @@ struct SliceWarp {
     using C = SliceCfg<S>;
     uint32_t lane, acc_s, q0_s, q1_s, q2_s, qc_s, T_s, R1_s, slots_s;
     uint32_t lane4, acc_lane_s;  // 4 * lane; acc_s + 4 * lane (the lane's word 0)
+    uint32_t planes_s;           // shared-window address of the staged planes (SMEM)
     const uint32_t* planes;  // shared (SMEM) or global
     const uint16_t* gslots;  // global slots (!SMEM)
     uint32_t vmask;          // this lane's real windows among its NWl
@@ -395,6 +402,7 @@ __device__ __forceinline__ SliceWarp<S, SMEM> slice_setup(const SliceArgs& a, ui
     }
     mbar_wait(bar, 0);
     w.planes = SMEM ? splanes : a.planes;
+    w.planes_s = smem_u32(splanes);
     w.gslots = a.slots;
     w.T_s = dyn_s;
     w.R1_s = dyn_s + 4u * kSR1Off;
@@ -432,12 +440,21 @@ template <int S, int LP, bool SMEM>
 __device__ __forceinline__ void slice_pass1(const SliceWarp<S, SMEM>& w, const uint32_t (&po)[LP],
                                             int i, uint32_t (&c)[5], uint32_t& r0m, uint32_t& r1m,
                                             uint32_t& r2m) {
-    const char* P = reinterpret_cast<const char*>(w.planes) + (size_t)i * (LP * 512);
     uint32_t m[LP];
+    if constexpr (SMEM) {  // one IMAD for the sequence, one IADD per plane
+        const uint32_t P = w.planes_s + (uint32_t)i * (uint32_t)(LP * 512);
 #pragma unroll
-    for (int j = 0; j < LP; ++j) {
-        PMS_CHECK(po[j] < (uint32_t)(LP * 512));
-        m[j] = *reinterpret_cast<const uint32_t*>(P + po[j]);
+        for (int j = 0; j < LP; ++j) {
+            PMS_CHECK(po[j] < (uint32_t)(LP * 512));
+            m[j] = lds32(P + po[j]);
+        }
+    } else {
+        const char* P = reinterpret_cast<const char*>(w.planes) + (size_t)i * (LP * 512);
+#pragma unroll
+        for (int j = 0; j < LP; ++j) {
+            PMS_CHECK(po[j] < (uint32_t)(LP * 512));
+            m[j] = __ldg(reinterpret_cast<const uint32_t*>(P + po[j]));
+        }
     }
     slice_count<LP>(m, w.km, c);
     const uint32_t hv = c[4] & w.vmask;
@@ -470,6 +487,32 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
 #pragma unroll
     for (int k = 0; k < C::KW; ++k) PMS_CHECK(lds32(w.acc_s + (k * 32u + lane) * 4u) == 0u);
     if (lane == 0) PMS_CHECK(lds32(w.qc_s) == 0u);
+#endif
+#if PMS_SLICE_R0_DIRECT
+    // r = 0 hits (~80 %) resolved by the finding lane, no queue: one slot load
+    // and one red per hit-iteration (~7 instructions) instead of a queue write
+    // and a share of a round (~16); the kernel is issue-bound, not LSU-bound
+    {
+        const uint32_t acc = w.acc_s;
+        while (r0m) {
+            const int q = msb(r0m);
+            r0m ^= 1u << q;
+            const uint32_t sl = slot_of(q);
+            red_or(acc | (sl & 0x7FFu), 1u << (sl >> 11));
+        }
+#if PMS_SLICE_R1_DIRECT
+        while (r1m) {
+            const int q = msb(r1m);
+            r1m ^= 1u << q;
+            const uint32_t sl = slot_of(q);
+            const uint32_t base = acc | (sl & 0x7FFu);
+            const uint32_t row = w.R1_s + (sl >> 11) * 64u;
+#pragma unroll
+            for (int u = 0; u < NU; ++u)
+                red_or(base ^ (r1_delta<X>((uint32_t)u) * 4u), lds32(row + (uint32_t)u * 4u));
+        }
+#endif
+    }
 #endif
     const uint32_t n012 =
         (uint32_t)__popc(r0m) | ((uint32_t)__popc(r1m) << 10) | ((uint32_t)__popc(r2m) << 20);

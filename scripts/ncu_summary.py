@@ -58,7 +58,7 @@ def full(rep: str, title: str) -> None:
         print()
 
 
-def to_json(rep: str, scans: int, out: str, kernel_note: str) -> None:
+def to_json(rep: str, scans: int, out: str, kernel_note: str, config: str = "") -> None:
     """The numbers bench.py's roofline object reads (profiles/slice_kernel_ncu.json):
     warp instructions per block scan (smsp__inst_executed.sum / the launch's
     block scans, from the same bench command's stats) and DRAM bytes per launch."""
@@ -76,6 +76,7 @@ def to_json(rep: str, scans: int, out: str, kernel_note: str) -> None:
         return float(vals[i].replace(",", "")) * scale
     inst = num("smsp__inst_executed.sum")
     doc = {"kernel": vals[hdr.index("Kernel Name")], "note": kernel_note,
+           "config": json.loads(config) if config else None,
            "source": os.path.relpath(rep) + " (ncu --set full --clock-control none)",
            "warp_instructions_per_launch": inst, "block_scans_per_launch": scans,
            "warp_instructions_per_scan": inst / scans,
@@ -123,6 +124,7 @@ if __name__ == "__main__":
     elif len(sys.argv) >= 3 and sys.argv[1] == "json":
         a = sys.argv
         to_json(a[2], int(a[a.index("--scans") + 1]), a[a.index("--out") + 1],
-                a[a.index("--note") + 1] if "--note" in a else "")
+                a[a.index("--note") + 1] if "--note" in a else "",
+                a[a.index("--config") + 1] if "--config" in a else "")
     else:
         raise SystemExit(__doc__)
