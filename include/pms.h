@@ -92,6 +92,12 @@ typedef struct pms_launch {
     int32_t wide_words;      /* 1 = 64-bit window words (two 32-bit bit
                                 planes) even for l <= 16; automatic for
                                 l > 16.  Same result                         */
+    int32_t seq_parallel;    /* PMS_ALGO_SLICE with few blocks: 1 = scan every
+                                (block, sequence) pair in parallel and AND
+                                the per-sequence masks (no sequential skip
+                                rule; a block whose AND is empty is skipped);
+                                -1 = never; 0 = auto (when there are fewer
+                                than 1/4 as many blocks as resident warps)   */
 } pms_launch;
 
 /* Kernel families (pms_launch.algo).  Every family returns the same set.
@@ -134,7 +140,8 @@ typedef struct pms_stats {
                                   each is W prefix compares serving 4^S
                                   candidates                                 */
     int32_t block_digits;      /* PMS_ALGO_BLOCK suffix digits S (0 if none) */
-    int32_t reserved;
+    int32_t mode_flags;        /* bit 0: the slice family ran sequence-
+                                  parallel (pms_launch.seq_parallel)        */
 } pms_stats;
 
 /* ---------------------------------------------------------------------

@@ -40,7 +40,8 @@ class Launch(ctypes.Structure):
                 ("force_generic", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
                 ("no_skip", ctypes.c_int32), ("algo", ctypes.c_int32),
                 ("block_digits", ctypes.c_int32), ("table_global", ctypes.c_int32),
-                ("handoff", ctypes.c_int32), ("wide_words", ctypes.c_int32)]
+                ("handoff", ctypes.c_int32), ("wide_words", ctypes.c_int32),
+                ("seq_parallel", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -52,7 +53,7 @@ class Stats(ctypes.Structure):
                 ("generic", ctypes.c_int32), ("table_in_smem", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_uint32), ("algo", ctypes.c_int32),
                 ("block_scans", ctypes.c_uint64), ("block_digits", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("mode_flags", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -145,6 +145,8 @@ const BlockKernel kBlockKernels[] = {
     {6, 0, pms_search_block<Bp32, 6, true, 0>, pms_search_block<Bp32, 6, false, 0>},
     PMS_NWB_LIST(PMS_BLK5) PMS_NWB_LIST(PMS_BLK6)};
 
+int kSliceThreadsFor(int S) { return S == 7 ? SliceCfg<7>::NT : SliceCfg<6>::NT; }
+
 // PMS_ALGO_SLICE instances (pms_slice.cu) and their roofline kernels
 // (pms_roof.cu): block digits S x prefix length LP = l - S
 const SliceKernel* find_slice_kernel(int S, int LP) {
@@ -330,6 +332,9 @@ struct pms_plan {
     int NWl = 0, LP = 0;
     uint32_t plane_bytes = 0, slot_bytes = 0;
     SliceFn sfn = nullptr;
+    int seqpar = 0;                 // sequence-parallel slice kernel (pms_search_slice_sp)
+    uint32_t* d_spmask = nullptr;   // its per-block masks and counters
+    uint32_t* d_spcnt = nullptr;
 };
 
 namespace {
@@ -348,6 +353,8 @@ void destroy_plan(pms_plan* p) {
     cudaFree(p->d_table);
     cudaFree(p->d_planes);
     cudaFree(p->d_slots);
+    cudaFree(p->d_spmask);
+    cudaFree(p->d_spcnt);
     if (!p->state_external) cudaFree(p->d_state);
     cudaFreeHost(p->h_state);
     for (cudaEvent_t e : p->ev)
@@ -432,8 +439,20 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
                      ball_bytes + p->plane_bytes + p->slot_bytes + fs.sharedSizeBytes <= (size_t)smem_optin;
         p->smem_bytes = (uint32_t)ball_bytes + (p->in_smem ? p->plane_bytes + p->slot_bytes : 0u);
         p->sfn = p->in_smem ? sk->fn_smem : sk->fn_global;
+        // sequence-parallel when the range has few blocks for the resident
+        // warps (auto: blocks < warps / 4; measured at (9,2): one block's
+        // sequential chain of scans is ~45 of the ~52 us)
+        const int warps_total = p->sms * (kSliceThreadsFor(S) / 32);
+        const unsigned long long nblk = 1ull << (2 * (l - S));
+        const SliceFn spf = slice_seqpar_kernel(S, l - S);
+        if (spf && p->in_smem && p->launch.seq_parallel >= 0 &&
+            (p->launch.seq_parallel == 1 || nblk * 4ull < (unsigned long long)warps_total) &&
+            nblk <= (1ull << 16)) {
+            p->seqpar = 1;
+            p->sfn = spf;
+        }
         p->G = 32; p->NW = p->NWl; p->generic = 0;
-        p->block = S == 7 ? SliceCfg<7>::NT : SliceCfg<6>::NT;
+        p->block = kSliceThreadsFor(S);
         p->d_ball = ensure_slice_ball_table(p->dev);
         cudaFuncAttributes fa{};
         int occ = 0;
@@ -450,6 +469,13 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
         if (p->launch.ctas_per_sm > 0) occ = std::min(occ, (int)p->launch.ctas_per_sm);
         p->grid = p->sms * occ;
         if (p->launch.grid_ctas > 0) p->grid = std::min((int)p->launch.grid_ctas, p->grid);
+        const size_t sp_words = p->seqpar ? (size_t)nblk * 32 * (1u << (2 * (S - 5))) : 0;
+        if (p->seqpar &&
+            (cudaMalloc(&p->d_spmask, sp_words * 4) != cudaSuccess ||
+             cudaMalloc(&p->d_spcnt, (size_t)nblk * 4) != cudaSuccess)) {
+            destroy_plan(p);
+            return fail_cuda(__LINE__);
+        }
         if (cudaMalloc(&p->d_table, p->tab_bytes) != cudaSuccess ||
             cudaMalloc(&p->d_planes, p->plane_bytes) != cudaSuccess ||
             cudaMalloc(&p->d_slots, p->slot_bytes) != cudaSuccess ||
@@ -670,6 +696,14 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
         sa.st = p->d_state; sa.epoch = p->epoch;
         sa.nout = reinterpret_cast<unsigned long long*>(d_count);
         sa.out = d_out; sa.cap = cap;
+        int sp_words = 0, sp_blocks = 0;
+        if (p->seqpar) {
+            sa.spmask = p->d_spmask;
+            sa.spcnt = p->d_spcnt;
+            sa.sp_blocks = (span + kUnit - 1) / kUnit;
+            sp_blocks = (int)sa.sp_blocks;
+            sp_words = sp_blocks * 32 * (1 << (2 * (p->S - 5)));
+        }
         if (cudaEventRecord(p->ev[0], s) != cudaSuccess) return fail_cuda(__LINE__);
         const SlicePackFn pack = slice_pack_kernel(p->S);
         const unsigned pack_y =
@@ -677,7 +711,8 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
         pack<<<dim3((unsigned)p->n, pack_y), kSlicePackThreads, 0, s>>>(
             d_seqs, p->n, p->t, p->l, p->W, p->NWl, p->LP, static_cast<uint32_t*>(p->d_planes),
             static_cast<uint16_t*>(p->d_slots), static_cast<uint32_t*>(p->d_table), p->d_state,
-            reinterpret_cast<unsigned long long*>(d_count), p->epoch);
+            reinterpret_cast<unsigned long long*>(d_count), p->epoch, p->d_spmask, p->d_spcnt,
+            sp_words, sp_blocks);
         const cudaError_t e_pack = cudaGetLastError();
         if (e_pack != cudaSuccess) return fail_cuda(__LINE__, e_pack);
         if (timed && cudaEventRecord(p->ev[1], s) != cudaSuccess) return fail_cuda(__LINE__);
@@ -768,6 +803,7 @@ void fill_stats(pms_plan* p, pms_stats* stats) {
     stats->algo = p->algo;
     stats->block_scans = p->h_state->block_scans;
     stats->block_digits = p->S;
+    stats->mode_flags = p->seqpar ? 1 : 0;
     stats->motifs = 0;
     stats->grid = p->grid;
     stats->block = p->block;

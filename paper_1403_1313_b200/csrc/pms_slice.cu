@@ -22,9 +22,26 @@ const pms::SliceKernel kSliceKernels[] = {PMS_LP_LIST(PMS_SLICE5) PMS_SLICE5(10)
                                           PMS_LP_LIST(PMS_SLICE6) PMS_SLICE6(10)
                                           PMS_LP_LIST(PMS_SLICE7)};
 
+// sequence-parallel instances (few blocks: small l), staged tables only
+struct SpKernel {
+    int S, LP;
+    pms::SliceFn fn;
+};
+#define PMS_SP(S, LP) {S, LP, pms_search_slice_sp<S, LP>},
+#define PMS_SP5(LP) PMS_SP(5, LP)
+#define PMS_SP6(LP) PMS_SP(6, LP)
+const SpKernel kSpKernels[] = {PMS_LP_LIST(PMS_SP5) PMS_SP5(10) PMS_SP5(11)
+                               PMS_LP_LIST(PMS_SP6) PMS_SP6(10)};
+
 }  // namespace
 
 namespace pms {
+
+SliceFn slice_seqpar_kernel(int S, int LP) {
+    for (const SpKernel& k : kSpKernels)
+        if (k.S == S && k.LP == LP) return k.fn;
+    return nullptr;
+}
 
 const SliceKernel* slice_kernels(int* count) {
     *count = (int)(sizeof(kSliceKernels) / sizeof(kSliceKernels[0]));

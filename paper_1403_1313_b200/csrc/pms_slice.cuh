@@ -61,6 +61,12 @@ struct SliceArgs {
     int batch, skip, handoff;
     int out_wide;
     uint32_t plane_bytes, slot_bytes;  // staged sizes (16-B multiples)
+    // sequence-parallel mode (pms_search_slice_sp): per block of the range, its
+    // candidate mask (32*KW words, ANDed over sequences) and a counter
+    // (completed units | kSpDead once the mask is empty)
+    uint32_t* spmask;
+    uint32_t* spcnt;
+    unsigned long long sp_blocks;
     DevState* st;
     uint32_t epoch;
     unsigned long long* nout;
@@ -70,7 +76,8 @@ struct SliceArgs {
 
 using SliceFn = void (*)(SliceArgs);
 using SlicePackFn = void (*)(const uint8_t*, int, int, int, int, int, int, uint32_t*, uint16_t*,
-                             uint32_t*, DevState*, unsigned long long*, uint32_t);
+                             uint32_t*, DevState*, unsigned long long*, uint32_t, uint32_t*,
+                             uint32_t*, int, int);
 using SliceRoofFn = void (*)(SliceArgs, int, unsigned long long, unsigned long long*);
 
 // Kernel instances, one translation unit each (pms_slice.cu, pms_roof.cu),
@@ -80,6 +87,7 @@ struct SliceKernel {
     SliceFn fn_smem, fn_global;
 };
 const SliceKernel* slice_kernels(int* count);              // pms_slice.cu
+SliceFn slice_seqpar_kernel(int S, int LP);                // pms_slice.cu (staged tables)
 SlicePackFn slice_pack_kernel(int S);                      // pms_slice.cu
 SliceRoofFn slice_roofline_kernel(int S, int LP, int mode, bool smem);  // pms_roof.cu
 int64_t debug_violations_slice(int reset);
@@ -98,6 +106,7 @@ constexpr int kSliceMaxLP = 11;              // l <= 16, S >= 5
 #ifndef PMS_SLICE_R1_DIRECT
 #define PMS_SLICE_R1_DIRECT 0  // r = 1 hits resolved per lane (NU reds each); 0: queued
 #endif
+constexpr uint32_t kSpDead = 0x80000000u;     // spcnt flag: the block's AND is empty
 constexpr uint32_t kPoison16 = 0xFFFFu;      // debug builds: consumed / unwritten queue entry
 constexpr uint32_t kPoison32 = 0xFFFFFFFFu;  // (no real entry: slots < 2^14, r < 16)
 constexpr int kSlicePackThreads = 256;
@@ -153,11 +162,18 @@ template <int S>
 __global__ void __launch_bounds__(kSlicePackThreads) pms_pack_slice(
     const uint8_t* __restrict__ seqs, int n, int t, int l, int W, int NWl, int LP,
     uint32_t* __restrict__ planes, uint16_t* __restrict__ slots, uint32_t* __restrict__ words,
-    DevState* st, unsigned long long* nout, uint32_t epoch) {
+    DevState* st, unsigned long long* nout, uint32_t epoch, uint32_t* spmask, uint32_t* spcnt,
+    int sp_words, int sp_blocks) {
     constexpr int X = S - 5;
     __shared__ uint8_t code[1024 + 32];
     pdl_launch_dependents();
     const int i = blockIdx.x;
+    if (sp_blocks) {  // sequence-parallel scratch: masks all ones, counters 0
+        const int g = (int)(blockIdx.x * gridDim.y + blockIdx.y) * kSlicePackThreads + (int)threadIdx.x;
+        const int gs = (int)(gridDim.x * gridDim.y) * kSlicePackThreads;
+        for (int x = g; x < sp_words; x += gs) spmask[x] = kFull;
+        for (int x = g; x < sp_blocks; x += gs) spcnt[x] = 0u;
+    }
     if (i == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
         *nout = 0ull;
         st->next = 0ull;
@@ -763,6 +779,95 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
         if (scanned) atomicAdd(&a.st->extra, scanned);
         if (bscans) atomicAdd(&a.st->block_scans, bscans);
     }
+}
+
+// ------------------------------------------- sequence-parallel search
+// For ranges with few blocks (e.g. (9,2): 256 blocks for 4,736 resident
+// warps), the sequential per-block chain of scans is the whole run time.
+// Here every (block, sequence) pair is its own work unit: a warp scans one
+// sequence for one block (alive starts full), ANDs the result into the
+// block's global mask, and the unit that completes the block's n-th sequence
+// emits the survivors.  The set is the definition's (AND over sequences of
+// "has a window within d"); the sequential skip rule is replaced by a dead
+// flag: once a block's AND is empty its remaining units skip the scan.
+template <int S, int LP>
+__global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice_sp(SliceArgs a) {
+    using B = BlkTraits<S>;
+    using C = SliceCfg<S>;
+    constexpr int KW = C::KW, NWARP = C::NWARP;
+    extern __shared__ __align__(128) uint32_t sdyn[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t qcnts[NWARP];
+    pdl_wait();
+    if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
+    const SliceWarp<S, true> w = slice_setup<S, true>(a, sdyn, &bar, qcnts);
+    const uint32_t lane = w.lane;
+    const unsigned long long nunits = a.sp_blocks * (unsigned long long)a.n;
+    unsigned long long bscans = 0;
+    for (;;) {
+        unsigned long long u = 0;
+        if (lane == 0) u = atomicAdd(&a.st->next, 1ull);
+        u = __shfl_sync(kFull, u, 0);
+        if (u >= nunits) break;
+        const unsigned long long b = u / (unsigned)a.n;
+        const int i = (int)(u - b * (unsigned)a.n);
+        const unsigned long long cbase = a.lo_al + (b << (2 * S));
+        uint32_t* gmask = a.spmask + b * (32ull * KW);
+        uint32_t flag = 0;
+        if (lane == 0) flag = *(volatile uint32_t*)&a.spcnt[b];
+        flag = __shfl_sync(kFull, flag, 0);
+        if (!(flag & kSpDead)) {
+            uint32_t po[LP];
+            slice_offsets<S, LP>(cbase, lane, po);
+            uint32_t alive[KW];
+#pragma unroll
+            for (int k = 0; k < KW; ++k) alive[k] = kFull;
+            if (cbase < a.lo || cbase + B::C > a.hi) {  // edge block of [lo, hi)
+#pragma unroll 1
+                for (int k = 0; k < KW; ++k) {
+                    uint32_t m = 0u;
+#pragma unroll 1
+                    for (uint32_t bb = 0; bb < 32; ++bb) {
+                        const unsigned long long c = cbase + blk_sfx<Bp32, S>(lane, k, bb);
+                        if (c >= a.lo && c < a.hi) m |= 1u << bb;
+                    }
+#pragma unroll
+                    for (int q = 0; q < KW; ++q)
+                        if (q == k) alive[q] = m;
+                }
+            }
+            uint32_t c[5], r0m, r1m, r2m, common = 0u;
+            slice_pass1<S, LP, true>(w, po, i, c, r0m, r1m, r2m);
+            slice_pass2<S, true>(w, i, c, r0m, r1m, r2m, common);
+            slice_finish<S, true>(w, common, alive, 0);
+            ++bscans;
+            uint32_t left = 0u;
+#pragma unroll
+            for (int k = 0; k < KW; ++k) left |= atomicAnd(gmask + k * 32 + lane, alive[k]) & alive[k];
+            if (!__any_sync(kFull, left != 0u) && lane == 0) atomicOr(&a.spcnt[b], kSpDead);
+        }
+        __threadfence();  // the AND is visible before this unit counts as done
+        uint32_t done = 0;
+        if (lane == 0) done = atomicAdd(&a.spcnt[b], 1u) & 0xFFFFu;
+        done = __shfl_sync(kFull, done, 0);
+        if (done == (uint32_t)a.n - 1u) {  // the block's last unit: emit its survivors
+            __threadfence();
+#pragma unroll
+            for (int k = 0; k < KW; ++k) {
+                const uint32_t m = __ldcg(gmask + k * 32 + lane);
+                if (!m) continue;
+                unsigned long long slot = atomicAdd(a.nout, (unsigned long long)__popc(m));
+                for (uint32_t mm = m; mm; mm &= mm - 1, ++slot) {
+                    const unsigned long long code = cbase + blk_sfx<Bp32, S>(lane, k, __ffs(mm) - 1);
+                    if (slot < a.cap) {
+                        if (a.out_wide) static_cast<unsigned long long*>(a.out)[slot] = code;
+                        else static_cast<uint32_t*>(a.out)[slot] = (uint32_t)code;
+                    }
+                }
+            }
+        }
+    }
+    if (lane == 0 && bscans) atomicAdd(&a.st->block_scans, bscans);
 }
 
 // ------------------------------------------------- roofline microbenchmark

@@ -212,3 +212,53 @@ def test_slice_compaction_stress(orc):
     assert r.stats.algo == pms.ALGO_SLICE
     assert r.status == 0 and r.count == want.count
     assert r.codes.tolist() == want.codes.tolist()
+
+
+# ------------------------------------------------- sequence-parallel mode
+
+def test_seq_parallel_auto_for_few_blocks():
+    """(9,2) has 256 blocks for 4,736 resident warps: AUTO runs every (block,
+    sequence) pair in parallel (pms_stats.mode_flags bit 0); (15,4) does not."""
+    g = json.load(open(os.path.join(GOLDEN, "bj0_seed1.json")))
+    s, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
+    r = pms.find_ex(s, g["l"], g["d"], max_out=1 << 20)
+    assert r.status == 0 and r.stats.algo == pms.ALGO_SLICE and r.stats.mode_flags & 1
+    assert r.codes.tolist() == g["codes"]
+    assert r.stats.block_scans <= 256 * 20  # dead blocks skip their remaining units
+    r2 = pms.find_ex(s, g["l"], g["d"], launch=slice_launch(seq_parallel=-1), max_out=1 << 20)
+    assert not (r2.stats.mode_flags & 1) and r2.codes.tolist() == g["codes"]
+    s3, _ = fmgen.generate_fm(20, 600, 15, 4, 1)
+    r3 = pms.find_ex(s3, 15, 4, lo=0, hi=1 << 24)
+    assert not (r3.stats.mode_flags & 1)
+
+
+@pytest.mark.parametrize("path", GOLDEN_FILES[:9], ids=[os.path.basename(p) for p in GOLDEN_FILES[:9]])
+def test_seq_parallel_forced_against_golden(orc, path):
+    g = json.load(open(path))
+    s, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
+    for S in (5, 6):
+        r = pms.find_ex(s, g["l"], g["d"], launch=slice_launch(S, seq_parallel=1), max_out=1 << 22)
+        assert r.status == 0 and r.count == g["count"] and r.codes.tolist() == g["codes"]
+        assert r.stats.mode_flags & 1
+
+
+def test_seq_parallel_tiny_random_and_ranges(orc):
+    rng = random.Random(909)
+    for trial in range(60):
+        S = rng.choice([5, 6])
+        l = rng.randint(S + 1, 11)
+        n = rng.randint(1, 8)
+        t = rng.randint(l, 160)
+        d = rng.randint(0, min(5, l - S - 1))
+        s = fmgen.random_sequences(n, t, 81000 + trial)
+        L = slice_launch(S, seq_parallel=1)
+        check(s, l, d, orc, launch=L, expect_slice=True)
+        lo = rng.randrange(0, 4 ** l)
+        hi = min(4 ** l, lo + rng.choice([1, 7, 1023, 1025, 5000, 70000]))
+        check(s, l, d, orc, lo=lo, hi=hi, launch=L)
+    # planted (9,2) instances: the consensus is among the survivors
+    for seed in range(4):
+        s, rec = fmgen.generate_fm(12, 300, 9, 2, 60 + seed)
+        got = check(s, 9, 2, orc, launch=slice_launch(5, seq_parallel=1), expect_slice=True)
+        code = int("".join(str("ACGT".index(c)) for c in rec.consensus), 4)
+        assert code in set(got.codes.tolist())
