@@ -257,8 +257,10 @@ int pms_roofline(int32_t iters, double *compares_per_s,
  * runs the plan's own per-scan code on the tables of its last execution
  * (pms_plan_execute*, completed or not: this call waits for it) with
  * everything dynamic removed -- no work counter, no skip rule, no hand-off,
- * no output; warp g scans block (g + k * warps) mod 4^(l-S) against sequence
- * (g + k) mod n for k < scans_per_warp, every warp busy throughout.
+ * no output; warp g walks consecutive blocks of its own region of the code
+ * space and scans each against sequences 0 .. D-1, D = the last execution's
+ * (block, sequence) scans per block (the mix the skip rule produced), for
+ * scans_per_warp scans, every warp busy throughout.
  *   mode 0: pass 1 only (plane loads + carry-save hit classification): R_pass1
  *   mode 1: pass 1 + hit resolution + end of scan at the instance's own hit
  *           mix: R_scan

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -1205,8 +1206,15 @@ extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_wa
         return PMS_E_ARG;
     const SliceRoofFn fn = slice_roofline_kernel(p->S, p->LP, mode, p->in_smem != 0);
     if (!fn) return PMS_E_ARG;
-    // the tables of the plan's last execution (its pre-pass) must be complete
-    if (cudaEventSynchronize(p->ev[2]) != cudaSuccess) return fail_cuda(__LINE__);
+    // the tables of the plan's last execution (its pre-pass) must be complete;
+    // its scans per block set the sequence mix the microbenchmark visits
+    DevState hs{};
+    if (cudaEventSynchronize(p->ev[2]) != cudaSuccess ||
+        cudaMemcpy(&hs, p->d_state, sizeof(hs), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail_cuda(__LINE__);
+    const double blocks_run =
+        std::max(1.0, std::ceil((double)(p->last_hi - p->last_lo) / (double)(1ull << (2 * p->S))));
+    const int depth = std::max(1, std::min(p->n, (int)std::llround((double)hs.block_scans / blocks_run)));
     int smem_optin = 0;
     cudaFuncAttributes fa{};
     if (cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->dev) !=
@@ -1228,7 +1236,8 @@ extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_wa
     float best = 1e30f;
     for (int r = 0; r < 4; ++r) {  // one warm-up, best of three
         cudaEventRecord(e0, s);
-        fn<<<p->grid, p->block, p->smem_bytes, s>>>(sa, r == 0 ? 1 : scans_per_warp, nblocks, sink);
+        fn<<<p->grid, p->block, p->smem_bytes, s>>>(sa, r == 0 ? 1 : scans_per_warp, depth, nblocks,
+                                                    sink);
         cudaEventRecord(e1, s);
         if (cudaEventSynchronize(e1) != cudaSuccess) break;
         float t = 0.f;

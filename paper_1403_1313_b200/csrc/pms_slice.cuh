@@ -78,7 +78,7 @@ using SliceFn = void (*)(SliceArgs);
 using SlicePackFn = void (*)(const uint8_t*, int, int, int, int, int, int, uint32_t*, uint16_t*,
                              uint32_t*, DevState*, unsigned long long*, uint32_t, uint32_t*,
                              uint32_t*, int, int);
-using SliceRoofFn = void (*)(SliceArgs, int, unsigned long long, unsigned long long*);
+using SliceRoofFn = void (*)(SliceArgs, int, int, unsigned long long, unsigned long long*);
 
 // Kernel instances, one translation unit each (pms_slice.cu, pms_roof.cu),
 // so they compile in parallel with pms.cu and pms64.cu.
@@ -873,13 +873,18 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice_sp(SliceA
 // ------------------------------------------------- roofline microbenchmark
 // The search kernel's per-scan code on the same tables, with everything
 // dynamic removed: no work counter, no skip rule, no hand-off, no output.
-// Warp g of the grid scans block (g + k * warps) mod nblocks against
-// sequence k mod n for k = 0 .. scans-1, every warp busy throughout.
+// Warp g walks consecutive blocks from its own region of the code space (as
+// the search's batches do: neighbouring blocks share all but the last prefix
+// digit, hence most plane rows) and scans each against sequences 0 ..
+// depth-1, depth = the last execution's scans per block (the mix the skip
+// rule produced); every warp stays busy for `scans` scans.  Both matter
+// when the tables are read through L1/L2.
 //   MODE 0: pass 1 only (plane loads + carry-save classification) -> R_pass1
 //   MODE 1: pass 1 + hit resolution + end of scan at the instance's own hit
 //           mix (alive reset each scan) -> R_scan
 template <int S, int LP, bool SMEM, int MODE>
 __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceArgs a, int scans,
+                                                                        int depth,
                                                                         unsigned long long nblocks,
                                                                         unsigned long long* sink) {
     using C = SliceCfg<S>;
@@ -891,8 +896,8 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
     const unsigned long long warps = (unsigned long long)gridDim.x * NWARP;
     const unsigned long long g = (unsigned long long)blockIdx.x * NWARP + (threadIdx.x >> 5);
     uint32_t acc = 0;
-    unsigned long long blk = g % nblocks;
-    int i = (int)(g % (unsigned long long)a.n);
+    unsigned long long blk = (g * ((nblocks + warps - 1) / warps)) % nblocks;
+    int i = 0;
 #pragma unroll 1
     for (int k = 0; k < scans; ++k) {
         uint32_t po[LP];
@@ -908,9 +913,10 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
             for (int q = 0; q < KW; ++q) alive[q] = kFull;
             acc += (uint32_t)slice_finish<S, SMEM>(w, common, alive, a.handoff);
         }
-        blk += warps;
-        if (blk >= nblocks) blk -= nblocks * (blk / nblocks);
-        if (++i == a.n) i = 0;
+        if (++i == depth) {
+            i = 0;
+            if (++blk == nblocks) blk = 0;
+        }
     }
     if (acc == 0x9E3779B9u) sink[0] = acc;  // keeps the work live
 }

@@ -14,7 +14,7 @@ for ci in range(5):
         for _ in range(3):
             plan.execute_tensors(s, out, cnt)
             st_, st = plan.wait()
-        live = st.issued_compares / (st.search_ms * 1e-3)
+        live = st.block_scans * (c['t'] - c['l'] + 1) / (st.search_ms * 1e-3)
         try:
             r0 = plan.roofline(0, 256); r1 = plan.roofline(1, 64)
             print(f"{c['name']:20s} S={st.block_digits} live {live/1e9:9.1f} Gtests/s  R_pass1 {r0['tests_per_s']/1e9:9.1f}  "
