@@ -98,6 +98,12 @@ typedef struct pms_launch {
                                 rule; a block whose AND is empty is skipped);
                                 -1 = never; 0 = auto (when there are fewer
                                 than 1/4 as many blocks as resident warps)   */
+    int32_t overlap_prepass; /* plan API: 1 = no timing event between the
+                                pre-pass and the search kernel, so the search
+                                (a programmatic dependent launch) overlaps the
+                                pre-pass's tail; pms_stats.pack_ms is then 0
+                                and search_ms covers both (pms_find* without
+                                stats always run this way)                   */
 } pms_launch;
 
 /* Kernel families (pms_launch.algo).  Every family returns the same set.

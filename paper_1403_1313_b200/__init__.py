@@ -41,7 +41,7 @@ class Launch(ctypes.Structure):
                 ("no_skip", ctypes.c_int32), ("algo", ctypes.c_int32),
                 ("block_digits", ctypes.c_int32), ("table_global", ctypes.c_int32),
                 ("handoff", ctypes.c_int32), ("wide_words", ctypes.c_int32),
-                ("seq_parallel", ctypes.c_int32)]
+                ("seq_parallel", ctypes.c_int32), ("overlap_prepass", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):

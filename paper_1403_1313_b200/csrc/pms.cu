@@ -327,6 +327,7 @@ struct pms_plan {
     int grid = 0, block = kBlock, batch = kSub;
     unsigned long long last_lo = 0, last_hi = 0;
     bool executed = false;
+    bool last_timed = true;       // the last execution recorded the pre-pass/search event
     // PMS_ALGO_SLICE (pms_slice.cuh): match planes, r = 0 slots, kernel
     void* d_planes = nullptr;
     void* d_slots = nullptr;
@@ -675,6 +676,7 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     p->batch = batch;
     p->last_lo = lo;
     p->last_hi = hi;
+    p->last_timed = timed;
 
     SearchArgs a{};
     a.tab = p->d_table; a.n = p->n; a.W = p->W; a.Wp = p->Wp;
@@ -771,12 +773,14 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
 
 extern "C" int pms_plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi,
                                 uint32_t* d_out, uint64_t cap, uint64_t* d_count, void* stream) {
-    return plan_execute(p, d_seqs, lo, hi, d_out, 0, cap, d_count, stream);
+    return plan_execute(p, d_seqs, lo, hi, d_out, 0, cap, d_count, stream,
+                        !(p && p->launch.overlap_prepass));
 }
 
 extern "C" int pms_plan_execute64(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi,
                                   uint64_t* d_out, uint64_t cap, uint64_t* d_count, void* stream) {
-    return plan_execute(p, d_seqs, lo, hi, d_out, 1, cap, d_count, stream);
+    return plan_execute(p, d_seqs, lo, hi, d_out, 1, cap, d_count, stream,
+                        !(p && p->launch.overlap_prepass));
 }
 
 namespace {
@@ -784,9 +788,13 @@ namespace {
 // Fill *stats from the plan's events and its (already read back) state.
 void fill_stats(pms_plan* p, pms_stats* stats) {
     float pack = 0.f, search = 0.f, tot = 0.f;
-    cudaEventElapsedTime(&pack, p->ev[0], p->ev[1]);
-    cudaEventElapsedTime(&search, p->ev[1], p->ev[2]);
     cudaEventElapsedTime(&tot, p->ev[0], p->ev[2]);
+    if (p->last_timed) {
+        cudaEventElapsedTime(&pack, p->ev[0], p->ev[1]);
+        cudaEventElapsedTime(&search, p->ev[1], p->ev[2]);
+    } else {
+        search = tot;  // (no boundary event: the two kernels overlap)
+    }
     stats->pack_ms = pack;
     stats->search_ms = search;
     stats->total_ms = tot;

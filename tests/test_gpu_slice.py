@@ -262,3 +262,25 @@ def test_seq_parallel_tiny_random_and_ranges(orc):
         got = check(s, 9, 2, orc, launch=slice_launch(5, seq_parallel=1), expect_slice=True)
         code = int("".join(str("ACGT".index(c)) for c in rec.consensus), 4)
         assert code in set(got.codes.tolist())
+
+
+def test_overlap_prepass_plan_parity(orc):
+    """pms_launch.overlap_prepass: no event between the pre-pass and the
+    search (they overlap through the programmatic dependent launch); the set
+    is unchanged and search_ms then covers both kernels."""
+    import torch
+    s, _ = fmgen.generate_fm(20, 600, 13, 3, 2)
+    want = orc.find(s, 13, 3).codes.tolist()
+    dev = torch.device("cuda", 0)
+    seqs = torch.from_numpy(s).to(dev)
+    out = torch.zeros(1 << 16, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    for ov in (0, 1):
+        with pms.Plan(20, 600, 13, 3, pms.Launch(overlap_prepass=ov)) as plan:
+            for _ in range(3):
+                plan.execute_tensors(seqs, out, cnt)
+                status, st = plan.wait()
+                assert status == 0
+                got = sorted(out[:int(cnt.item())].cpu().numpy().astype(np.uint32).tolist())
+                assert got == want
+                assert (st.pack_ms == 0.0) == bool(ov) and st.search_ms > 0.0

@@ -55,13 +55,14 @@ def kernel_ms(seqs, l, d, launch=None, reps=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
-    ap.add_argument("--algo", choices=["auto", "candidate", "block"], default="auto")
+    ap.add_argument("--algo", choices=["auto", "candidate", "block", "slice"], default="auto")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
     global ALGO
-    ALGO = {"auto": pms.ALGO_AUTO, "candidate": pms.ALGO_CANDIDATE, "block": pms.ALGO_BLOCK}[args.algo]
+    ALGO = {"auto": pms.ALGO_AUTO, "candidate": pms.ALGO_CANDIDATE, "block": pms.ALGO_BLOCK,
+            "slice": pms.ALGO_SLICE}[args.algo]
     if args.out is None:
-        args.out = os.path.join(ROOT, "profiles", f"r01_experiments_{args.algo}")
+        args.out = os.path.join(ROOT, "profiles", f"r02_experiments_{args.algo}")
     pms.build()
     res = {"device": pms.device_info(), "algo": args.algo, "lsweep": [], "paper_instances": [],
            "workers": {}, "cpu_threads": {}}
