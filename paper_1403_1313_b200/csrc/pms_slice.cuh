@@ -118,7 +118,11 @@ struct SliceCfg {
     static constexpr int X = S - 5;
     static constexpr int KW = 1 << (2 * X);   // mask words per lane
     static constexpr int NU = 6 + 3 * X;      // words of a radius-1 ball
-    static constexpr int HPR = 32 / NU;       // r = 1 hits per round
+    // r = 1 rounds in two loops: (A) the own word + the 5 lane flips (R1 row
+    // bits), 5 hits per round; (B) the 3X words one upper position away (the
+    // centre bit, no table load), 32 / 3X hits per round
+    static constexpr int NUA = 6, HPRA = 32 / NUA;
+    static constexpr int NUB = 3 * X, HPRB = NUB ? 32 / NUB : 0;
 #ifndef PMS_SLICE7_NT
 #define PMS_SLICE7_NT 1024
 #endif
@@ -372,7 +376,7 @@ template <int S, bool SMEM>
 __device__ __forceinline__ SliceWarp<S, SMEM> slice_setup(const SliceArgs& a, uint32_t* sdyn,
                                                          uint64_t* bar, uint32_t* qcnts) {
     using C = SliceCfg<S>;
-    constexpr int X = C::X, KW = C::KW, NU = C::NU, HPR = C::HPR;
+    constexpr int X = C::X, KW = C::KW;
     SliceWarp<S, SMEM> w;
     w.lane = threadIdx.x & 31u;
     const uint32_t wid = threadIdx.x >> 5;
@@ -426,11 +430,11 @@ __device__ __forceinline__ SliceWarp<S, SMEM> slice_setup(const SliceArgs& a, ui
     for (int b = 0; b < 4; ++b) w.km[b] = a.kmask[b];
     const int nvalid = min(a.NWl, max(0, a.W - (int)w.lane * a.NWl));
     w.vmask = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
-    w.uL = w.lane % NU;
-    w.hL = w.lane / NU;
+    w.uL = w.lane % C::NUA;
+    w.hL = w.lane / C::NUA;
     w.dword4 = r1_delta<X>(w.uL) * 4u;
     w.r1row = w.R1_s + w.uL * 4u;
-    w.r1lane = w.lane < (uint32_t)(HPR * NU);
+    w.r1lane = w.lane < (uint32_t)(C::HPRA * C::NUA);
     w.NWl = a.NWl;
     w.Wp = a.Wp;
     return w;
@@ -487,7 +491,7 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
                                             const uint32_t (&c)[5], uint32_t r0m, uint32_t r1m,
                                             uint32_t r2m, uint32_t& common) {
     using C = SliceCfg<S>;
-    constexpr int X = C::X, NU = C::NU, HPR = C::HPR;
+    constexpr int X = C::X, NU = C::NU;
     const uint32_t lane = w.lane;
     // slot row of this lane's windows in sequence i
     const uint32_t srow = (uint32_t)(i * w.Wp) + lane * (uint32_t)w.NWl;
@@ -581,12 +585,26 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
             }
         }
 #pragma unroll 1
-        for (uint32_t b1 = 0; b1 < t1; b1 += HPR, qa1 += 2u * HPR) {
-            if (b1 + w.hL < r1lim) {
+        for (uint32_t b1 = 0; b1 < t1; b1 += C::HPRA, qa1 += 2u * C::HPRA) {
+            if (b1 + w.hL < r1lim) {  // (A) own word + lane flips
                 const uint32_t sl = lds16(qa1);
                 PMS_CHECK(sl != kPoison16);
                 // (acc | off) ^ d == (acc ^ d) | off: d and off lie inside the block
                 red_or(acc_d ^ (sl & 0x7FFu), lds32(r1row + (sl >> 11) * 64u));
+            }
+        }
+        if constexpr (X >= 1) {  // (B) the words one upper position away: centre bit
+            const uint32_t uB = lane % C::NUB, hB = lane / C::NUB;
+            uint32_t accB = w.acc_s ^ (r1_delta<X>(6u + uB) * 4u), qb = w.q1_s + 2u * hB;
+            asm volatile("" : "+r"(accB), "+r"(qb));
+            const uint32_t limB = lane < (uint32_t)(C::HPRB * C::NUB) ? t1 : 0u;
+#pragma unroll 1
+            for (uint32_t b1 = 0; b1 < t1; b1 += C::HPRB, qb += 2u * C::HPRB) {
+                if (b1 + hB < limB) {
+                    const uint32_t sl = lds16(qb);
+                    PMS_CHECK(sl != kPoison16);
+                    red_or(accB ^ (sl & 0x7FFu), 1u << (sl >> 11));
+                }
             }
         }
         __syncwarp();
