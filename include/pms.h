@@ -82,8 +82,8 @@ typedef struct pms_launch {
     int32_t block_digits;    /* block families' suffix digits S (5: 1024-,
                                 6: 4096-, 7: 16384-candidate blocks; 7 only
                                 in PMS_ALGO_SLICE); 0 = auto (slice: 7 if
-                                l >= 14, 6 if l = 13, else 5; block: 6 if
-                                l >= 13, else 5)                             */
+                                l >= 13, else 5; block: 6 if l >= 13,
+                                else 5)                                      */
     int32_t table_global;    /* 1 = read the packed table from global memory
                                 (L1/L2) instead of staging it in smem        */
     int32_t handoff;         /* block family: a block with at most this many

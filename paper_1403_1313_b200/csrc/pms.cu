@@ -407,13 +407,13 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     int S = p->launch.block_digits == 5 || p->launch.block_digits == 6 ? p->launch.block_digits
                                                                         : (l >= 13 ? 6 : 5);
     if (S > l) S = 5;
-    // slice family: S = 7 (16384-candidate blocks, slice family only) once
-    // there are >= 4^7 blocks to spread over the 4,736 resident warps (l >=
-    // 14; measured at (15,4): 203 us vs 326 us at S = 6; at (11,3) S = 7
-    // leaves most warps idle: 425 us vs 49 us), else the block family's rule
+    // slice family: S = 7 (16384-candidate blocks, slice family only) from
+    // l = 13 (measured: (15,4) 168 us vs 328 at S = 6, (13,3) 48 vs 51; at
+    // (11,3) S = 7 leaves most warps idle: 343 us vs 45), else the block
+    // family's rule
     const int S_slice = p->launch.block_digits >= 5 && p->launch.block_digits <= 7
                             ? p->launch.block_digits
-                            : (l >= 14 ? 7 : S);
+                            : (l >= 13 ? 7 : S);
     // PMS_ALGO_SLICE (the default where it applies): 32-bit codes, rows of at
     // most 1024 windows, a prefix of 1..11 digits with d below its length
     // (otherwise every window would hit); elsewhere the block family runs

@@ -46,7 +46,7 @@ def auto_algo(t, l, d):
     CANDIDATE."""
     if l < 5:
         return pms.ALGO_CANDIDATE
-    S = 7 if l >= 14 else 6 if l >= 13 else 5
+    S = 7 if l >= 13 else 5
     lp = l - S
     if l <= 16 and t - l + 1 <= 1024 and lp >= 1 and d < lp:
         return pms.ALGO_SLICE

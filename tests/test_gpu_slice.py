@@ -69,7 +69,7 @@ def test_slice_baseline_configs_against_golden(orc, path, S):
     assert rec.consensus == g["consensus"]
     r = pms.find_ex(s, g["l"], g["d"], launch=slice_launch(S), max_out=1 << 22)
     assert r.status == 0
-    S_ran = S or (7 if g["l"] >= 14 else 6 if g["l"] >= 13 else 5)
+    S_ran = S or (7 if g["l"] >= 13 else 5)
     assert (r.stats.algo == pms.ALGO_SLICE) == applies(g["t"], g["l"], g["d"], S_ran)
     assert r.count == g["count"] and r.codes.tolist() == g["codes"]
 
@@ -154,7 +154,7 @@ def test_slice_ineligible_d_and_auto(orc):
                          (2, 30, 13, 7), (2, 30, 13, 6), (5, 80, 11, 2), (2, 30, 14, 6),
                          (2, 30, 14, 7), (3, 40, 15, 4)]:
         s = fmgen.random_sequences(n, t, l * 10 + d)
-        S = 7 if l >= 14 else 6 if l >= 13 else 5
+        S = 7 if l >= 13 else 5
         check(s, l, d, orc, expect_slice=applies(t, l, d, S))
 
 
