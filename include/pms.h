@@ -147,7 +147,9 @@ typedef struct pms_stats {
                                   candidates                                 */
     int32_t block_digits;      /* PMS_ALGO_BLOCK suffix digits S (0 if none) */
     int32_t mode_flags;        /* bit 0: the slice family ran sequence-
-                                  parallel (pms_launch.seq_parallel)        */
+                                  parallel (pms_launch.seq_parallel);
+                                  bit 1: its hand-off checks ran on the
+                                  staged tables (few blocks per warp)       */
 } pms_stats;
 
 /* ---------------------------------------------------------------------

@@ -15,7 +15,8 @@ LIB = LIB_DEBUG if os.environ.get("PMS_DEBUG_LIB") == "1" else LIB_RELEASE
 LIB = os.environ.get("PMS_LIB_OVERRIDE") or LIB
 # pms.cu: 32-bit-word kernels + host code; pms64.cu: 64-bit-word kernels (l <= 31);
 # pms_slice.cu / pms_roof.cu: the slice family's kernels and roofline kernels
-SOURCES = [os.path.join(CSRC, f) for f in ("pms.cu", "pms64.cu", "pms_slice.cu", "pms_roof.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("pms.cu", "pms64.cu", "pms_slice.cu",
+                                              "pms_slice_ht.cu", "pms_roof.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, h) for h in ("pms_device.cuh", "pms_kernels.cuh",
                                                     "pms_slice.cuh")] + \
     [os.path.join(ROOT, "include", "pms.h")]

@@ -334,6 +334,8 @@ struct pms_plan {
     int NWl = 0, LP = 0;
     uint32_t plane_bytes = 0, slot_bytes = 0;
     SliceFn sfn = nullptr;
+    SliceFn sfn_ht = nullptr;  // the same search, hand-off on the staged tables (few blocks)
+    int last_ht = 0;
     int seqpar = 0;                 // sequence-parallel slice kernel (pms_search_slice_sp)
     uint32_t* d_spmask = nullptr;   // its per-block masks and counters
     uint32_t* d_spcnt = nullptr;
@@ -453,9 +455,19 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
             p->seqpar = 1;
             p->sfn = spf;
         }
+        if (p->in_smem && !p->seqpar) p->sfn_ht = slice_ht_kernel(S, l - S);
         p->G = 32; p->NW = p->NWl; p->generic = 0;
         p->block = kSliceThreadsFor(S);
         p->d_ball = ensure_slice_ball_table(p->dev);
+        cudaFuncAttributes fh{};
+        if (p->sfn_ht &&
+            (cudaFuncGetAttributes(&fh, (const void*)p->sfn_ht) != cudaSuccess ||
+             p->smem_bytes + fh.sharedSizeBytes > (size_t)smem_optin ||
+             cudaFuncSetAttribute((const void*)p->sfn_ht, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem_optin - (int)fh.sharedSizeBytes) != cudaSuccess)) {
+            destroy_plan(p);
+            return fail_cuda(__LINE__);
+        }
         cudaFuncAttributes fa{};
         int occ = 0;
         if (!p->d_ball || cudaFuncGetAttributes(&fa, (const void*)p->sfn) != cudaSuccess ||
@@ -699,6 +711,13 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
         sa.st = p->d_state; sa.epoch = p->epoch;
         sa.nout = reinterpret_cast<unsigned long long*>(d_count);
         sa.out = d_out; sa.cap = cap;
+        // hand-off checks on the staged tables (the HT instance) when the
+        // range has fewer than two blocks per resident warp (measured: (13,3)
+        // 48 -> 35 us); with many blocks per warp the packed-word check's
+        // fewer instructions win.  PMS_HANDOFF_TABLES=0/1 forces either.
+        static const char* ht_env = std::getenv("PMS_HANDOFF_TABLES");
+        const bool ht = p->sfn_ht && (ht_env ? std::atoi(ht_env) != 0 : span / kUnit < 2ull * warps);
+        p->last_ht = ht ? 1 : 0;
         int sp_words = 0, sp_blocks = 0;
         if (p->seqpar) {
             sa.spmask = p->d_spmask;
@@ -730,7 +749,7 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
             attr[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = attr;
             cfg.numAttrs = no_pdl ? 0 : 1;
-            const cudaError_t e = cudaLaunchKernelEx(&cfg, p->sfn, sa);
+            const cudaError_t e = cudaLaunchKernelEx(&cfg, ht ? p->sfn_ht : p->sfn, sa);
             if (e != cudaSuccess) return fail_cuda(__LINE__, e);
         }
         if (cudaEventRecord(p->ev[2], s) != cudaSuccess) return fail_cuda(__LINE__);
@@ -812,7 +831,7 @@ void fill_stats(pms_plan* p, pms_stats* stats) {
     stats->algo = p->algo;
     stats->block_scans = p->h_state->block_scans;
     stats->block_digits = p->S;
-    stats->mode_flags = p->seqpar ? 1 : 0;
+    stats->mode_flags = (p->seqpar ? 1 : 0) | (p->last_ht ? 2 : 0);
     stats->motifs = 0;
     stats->grid = p->grid;
     stats->block = p->block;

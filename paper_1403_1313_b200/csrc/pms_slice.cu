@@ -68,3 +68,12 @@ int64_t debug_violations_slice(int reset) {
 }
 
 }  // namespace pms
+
+#ifdef PMS_TRACE
+// tuning builds only: copy the per-warp trace of the last slice search launch
+extern "C" int pms_trace_read(unsigned long long* host, int nwarps) {
+    if (nwarps > 8192) nwarps = 8192;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    return cudaMemcpyFromSymbol(host, g_pms_trace, (size_t)nwarps * 64) == cudaSuccess ? 0 : -1;
+}
+#endif

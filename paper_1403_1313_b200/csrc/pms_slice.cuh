@@ -88,6 +88,8 @@ struct SliceKernel {
 };
 const SliceKernel* slice_kernels(int* count);              // pms_slice.cu
 SliceFn slice_seqpar_kernel(int S, int LP);                // pms_slice.cu (staged tables)
+SliceFn slice_ht_kernel(int S, int LP);                    // pms_slice_ht.cu (staged tables,
+                                                           // hand-off on the tables)
 SlicePackFn slice_pack_kernel(int S);                      // pms_slice.cu
 SliceRoofFn slice_roofline_kernel(int S, int LP, int mode, bool smem);  // pms_roof.cu
 int64_t debug_violations_slice(int reset);
@@ -151,6 +153,18 @@ struct SliceCfg {
 namespace {
 
 using namespace pms;
+
+#ifdef PMS_TRACE
+// tuning builds only (scripts/trace_tail.py): per warp of the last search
+// launch [enter, ready, end (globaltimer ns), blocks, scans, hand-off
+// candidates, most scans of one block, longest block (ns)]
+__device__ unsigned long long g_pms_trace[8192 * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 // ------------------------------------------------------------- pre-pass
 // Grid (n, G): CTA (i, y) stages sequence i's 2-bit codes in shared memory
@@ -684,7 +698,49 @@ __device__ __forceinline__ int slice_finish(const SliceWarp<S, SMEM>& w, uint32_
     return __reduce_add_sync(kFull, na);
 }
 
+// Hand-off check of one candidate (the block's prefix P and the suffix in
+// word k, lane `src`, bit `bit` of the block's mask) against sequences i0..n-1
+// on the scan's own tables (per candidate, skip rule): P x
+// matches sequence i iff some window w with prefix distance p <= d -- a
+// pass-1 hit -- has Hamming(x, e_w) <= r = d - p.  The slot of a window holds
+// its suffix planes (word k = eH>>5 << X | eL>>5, lane = eH & 31, bit =
+// eL & 31), so slot ^ slot(x) gives the suffix mismatches directly.  Staged
+// tables: no global-memory round trip per sequence (the packed-word check
+// was ~2 us per sequence of L2 latency on a lone warp, the (13,3) tail).
+template <int S>
+__device__ __forceinline__ uint32_t slice_sfx_dist(uint32_t v) {
+    constexpr int X = S - 5;
+    uint32_t mm = ((v >> 2) | (v >> 11)) & 31u;
+    if constexpr (X > 0) mm |= (((v >> 7) | (v >> (7 + X))) & ((1u << X) - 1u)) << 5;
+    return (uint32_t)__popc(mm);
+}
+
 template <int S, int LP, bool SMEM>
+__device__ __forceinline__ bool slice_check_one(const SliceWarp<S, SMEM>& w, const uint32_t (&po)[LP],
+                                                int i0, int n, uint32_t k, uint32_t src,
+                                                uint32_t bit, unsigned long long& scanned) {
+    const uint32_t sx = ((k * 32u + src) * 4u) | (bit << 11);
+    for (int i = i0; i < n; ++i) {
+        uint32_t c[5], r0m, r1m, r2m;
+        slice_pass1<S, LP, SMEM>(w, po, i, c, r0m, r1m, r2m);
+        ++scanned;
+        const uint32_t srow = (uint32_t)(i * w.Wp) + w.lane * (uint32_t)w.NWl;
+        bool f = false;
+        uint32_t hv = r0m | r1m | r2m;
+        while (hv && !f) {
+            const int q = msb(hv);
+            hv ^= 1u << q;
+            PMS_CHECK((int)w.lane * w.NWl + q < w.Wp);
+            const uint32_t sl = SMEM ? lds16(w.slots_s + 2u * (srow + (uint32_t)q))
+                                     : (uint32_t)__ldg(w.gslots + srow + (uint32_t)q);
+            f = slice_sfx_dist<S>(sl ^ sx) <= slice_r(c, q);
+        }
+        if (!__any_sync(kFull, f)) return false;
+    }
+    return true;
+}
+
+template <int S, int LP, bool SMEM, bool HT = false>
 __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs a) {
     using B = BlkTraits<S>;
     using C = SliceCfg<S>;
@@ -698,11 +754,18 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
     extern __shared__ __align__(128) uint32_t sdyn[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t qcnts[NWARP];
+#ifdef PMS_TRACE
+    const unsigned long long tr_enter = gtimer();
+    unsigned long long tr_blocks = 0, tr_hand = 0, tr_maxs = 0, tr_maxt = 0;
+#endif
     pdl_wait();
     if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
     const SliceWarp<S, SMEM> w = slice_setup<S, SMEM>(a, sdyn, &bar, qcnts);
     const uint32_t lane = w.lane;
     unsigned long long scanned = 0, bscans = 0;
+#ifdef PMS_TRACE
+    const unsigned long long tr_ready = gtimer();
+#endif
 
     for (;;) {
         unsigned long long bgrab = 0;
@@ -712,6 +775,20 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
         for (int sb = 0; sb < a.batch; sb += B::C) {
             const unsigned long long cbase = a.lo_al + bgrab + sb;
             if (cbase >= a.hi) break;
+#ifdef PMS_TRACE
+            const unsigned long long tr_b0 = gtimer(), tr_s0 = bscans, tr_h0 = scanned;
+            struct TrEnd {
+                unsigned long long t0, s0, h0, *maxs, *maxt, *blocks, *hand;
+                const unsigned long long *bs, *sc;
+                __device__ ~TrEnd() {
+                    const unsigned long long dt = gtimer() - t0;
+                    if (*bs - s0 > *maxs) *maxs = *bs - s0;
+                    if (dt > *maxt) *maxt = dt;
+                    ++*blocks;
+                    *hand += *sc - h0;
+                }
+            } tr_end{tr_b0, tr_s0, tr_h0, &tr_maxs, &tr_maxt, &tr_blocks, &tr_hand, &bscans, &scanned};
+#endif
             uint32_t po[LP];
             slice_offsets<S, LP>(cbase, lane, po);
             uint32_t alive[KW];
@@ -780,8 +857,16 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
                         if (q == (int)k) alive[q] &= alive[q] - 1;
                 }
                 const unsigned long long code = cbase + blk_sfx<Bp32, S>(src, k, pk & 31u);
-                if (check_sequences<Bp32>(a.words, i, a.n, a.Wp, Bp32::prep(code), a.dp, (int)lane,
-                                          scanned)) {
+                // HT (few blocks per warp: latency-bound, a lone warp's chain is
+                // the run time): the check on the staged tables; else the packed
+                // words (fewer instructions, L2 latency hidden by other warps)
+                bool ok;
+                if constexpr (HT)
+                    ok = slice_check_one<S, LP, SMEM>(w, po, i, a.n, k, (uint32_t)src, pk & 31u, scanned);
+                else
+                    ok = check_sequences<Bp32>(a.words, i, a.n, a.Wp, Bp32::prep(code), a.dp, (int)lane,
+                                               scanned);
+                if (ok) {
                     if (lane == 0) {
                         const unsigned long long slot = atomicAdd(a.nout, 1ull);
                         if (slot < a.cap) {
@@ -797,6 +882,14 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
         if (scanned) atomicAdd(&a.st->extra, scanned);
         if (bscans) atomicAdd(&a.st->block_scans, bscans);
     }
+#ifdef PMS_TRACE
+    const unsigned long long wg = (unsigned long long)blockIdx.x * NWARP + (threadIdx.x >> 5);
+    if (lane == 0 && wg < 8192) {
+        unsigned long long* r = g_pms_trace + wg * 8;
+        r[0] = tr_enter; r[1] = tr_ready; r[2] = gtimer(); r[3] = tr_blocks;
+        r[4] = bscans; r[5] = tr_hand; r[6] = tr_maxs; r[7] = tr_maxt;
+    }
+#endif
 }
 
 // ------------------------------------------- sequence-parallel search

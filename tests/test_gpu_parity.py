@@ -631,3 +631,48 @@ print("ok")
     p = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=300)
     assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("force", ["0", "1"])
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_handoff_check_kinds(cfg, force):
+    """The slice family's two hand-off checks -- on the staged
+    planes and slots (chosen for ranges with few blocks per warp) and on the
+    packed words -- each forced in a fresh process (PMS_HANDOFF_TABLES is read
+    once), give the golden set of (11,3), (13,3) and (15,4); mode_flags bit 1
+    reports the kind that ran.  With the default, (13,3) (4,096 blocks for
+    4,736 warps) runs the tables check and (15,4) the packed-word one."""
+    import subprocess
+    import sys
+    path = os.path.join(GOLDEN, f"bj{cfg}_seed1.json")
+    code = f"""
+import json, sys
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import fmgen, paper_1403_1313_b200 as pms
+g = json.load(open({path!r}))
+s, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
+r = pms.find_ex(s, g["l"], g["d"])
+assert r.status == 0 and r.codes.tolist() == g["codes"], r.status
+assert r.stats.algo == pms.ALGO_SLICE
+assert (r.stats.mode_flags >> 1) & 1 == {int(force)}, r.stats.mode_flags
+lo, hi = 4 ** g["l"] // 3, 4 ** g["l"] // 3 + 3 * 4 ** (g["l"] - 3) + 777
+r = pms.find_ex(s, g["l"], g["d"], lo=lo, hi=hi)
+want = [c for c in g["codes"] if lo <= c < hi]
+assert r.status == 0 and r.codes.tolist() == want
+print("ok")
+"""
+    p = subprocess.run([sys.executable, "-c", code],
+                       env={**os.environ, "PMS_HANDOFF_TABLES": force},
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stderr[-2000:]
+
+
+def test_handoff_kind_default_by_blocks_per_warp():
+    """Default choice of the hand-off check: staged tables below two blocks per
+    resident warp ((13,3): 4,096 blocks), packed words above ((15,4): 65,536)."""
+    for cfg, want in ((2, 1), (3, 0)):
+        g = json.load(open(os.path.join(GOLDEN, f"bj{cfg}_seed1.json")))
+        s, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
+        r = pms.find_ex(s, g["l"], g["d"])
+        assert r.status == 0 and r.codes.tolist() == g["codes"]
+        assert (r.stats.mode_flags >> 1) & 1 == want, (cfg, r.stats.mode_flags)
