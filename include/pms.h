@@ -67,7 +67,8 @@ enum {
 typedef struct pms_launch {
     int32_t ctas_per_sm;     /* persistent CTAs per SM (grid = SMs * this)   */
     int32_t warps_per_cta;   /* warps per CTA                                */
-    int32_t batch;           /* candidates per atomic grab (multiple of 256) */
+    int32_t batch;           /* candidates per atomic grab (multiple of 256;
+                                0 = auto: one block for the slice family)   */
     int32_t lanes_per_cand;  /* 16 or 32 lanes per candidate, 0 = pick the
                                 one with less window padding                 */
     int32_t force_generic;   /* 1 = windows never register-resident          */

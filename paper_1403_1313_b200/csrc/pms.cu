@@ -679,7 +679,9 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
     // batch: aim for >= 8 grabs per warp, multiple of kSub, at most 16 sub-blocks
     const unsigned long long warps = (unsigned long long)p->grid * (p->block / 32);
     int batch = p->launch.batch > 0 ? (int)((p->launch.batch + kUnit - 1) / kUnit * kUnit) : 0;
-    if (batch == 0) {
+    if (batch == 0 && p->algo == PMS_ALGO_SLICE) {
+        batch = (int)kUnit;  // one block per grab (measured: (16,5) -1.4 %, (15,4) equal)
+    } else if (batch == 0) {
         unsigned long long b = span / (warps * 8);
         b = (b + kUnit - 1) / kUnit * kUnit;
         batch = (int)std::min<unsigned long long>(std::max<unsigned long long>(b, kUnit),

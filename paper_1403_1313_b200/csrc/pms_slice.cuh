@@ -105,6 +105,9 @@ constexpr int kSliceMaxLP = 11;              // l <= 16, S >= 5
 #ifndef PMS_SLICE_R0_DIRECT
 #define PMS_SLICE_R0_DIRECT 1  // r = 0 hits resolved per lane (no queue); 0: queued
 #endif
+#ifndef PMS_SLICE_EXCH
+#define PMS_SLICE_EXCH 1  // end of scan: atom.exch(word, 0) instead of load + store
+#endif
 #ifndef PMS_SLICE_R1_DIRECT
 #define PMS_SLICE_R1_DIRECT 0  // r = 1 hits resolved per lane (NU reds each); 0: queued
 #endif
@@ -316,6 +319,11 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
 }
 __device__ __forceinline__ void red_or(uint32_t a, uint32_t v) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_exch0(uint32_t a) {
+    uint32_t r;
+    asm volatile("atom.shared.exch.b32 %0, [%1], 0;" : "=r"(r) : "r"(a) : "memory");
+    return r;
 }
 __device__ __forceinline__ uint32_t atom_add(uint32_t a, uint32_t v) {
     uint32_t r;
@@ -685,8 +693,12 @@ __device__ __forceinline__ int slice_finish(const SliceWarp<S, SMEM>& w, uint32_
 #pragma unroll
     for (int k = 0; k < KW; ++k) {
         const uint32_t wa = w.acc_s + (k * 32u + w.lane) * 4u;
+#if PMS_SLICE_EXCH
+        alive[k] &= atom_exch0(wa) | common;  // read and clear in one instruction
+#else
         alive[k] &= lds32(wa) | common;
         sts32(wa, 0u);
+#endif
         any |= alive[k];
     }
     __syncwarp();

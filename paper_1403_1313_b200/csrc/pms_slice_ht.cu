@@ -37,3 +37,12 @@ SliceFn slice_ht_kernel(int S, int LP) {
 }
 
 }  // namespace pms
+
+#ifdef PMS_TRACE
+// tuning builds only: the trace of this translation unit's instances
+extern "C" int pms_trace_read_ht(unsigned long long* host, int nwarps) {
+    if (nwarps > 8192) nwarps = 8192;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    return cudaMemcpyFromSymbol(host, g_pms_trace, (size_t)nwarps * 64) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -36,6 +36,7 @@ import paper_1403_1313_b200 as pms  # noqa: E402
 
 L = pms.load()
 L.pms_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
+L.pms_trace_read_ht.argtypes = [ctypes.c_void_p, ctypes.c_int]
 dev = torch.device("cuda", 0)
 out = torch.zeros(1 << 20, dtype=torch.int32, device=dev)
 cnt = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -56,7 +57,10 @@ for ci in [int(x) for x in args.configs.split(",")]:
                     ms.append(st.search_ms)
             nw = st.grid * st.block // 32
             buf = np.zeros((8192, 8), dtype=np.uint64)
-            assert L.pms_trace_read(buf.ctypes.data, nw) == 0
+            # the instance that ran (mode_flags bit 1: the hand-off-on-tables
+            # one, its own translation unit and trace buffer)
+            rd = L.pms_trace_read_ht if (st.mode_flags >> 1) & 1 else L.pms_trace_read
+            assert rd(buf.ctypes.data, nw) == 0
             tr = buf[:nw].astype(np.int64)
             t0 = tr[:, 0].min()
             enter, ready, end = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3
