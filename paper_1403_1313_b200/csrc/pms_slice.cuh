@@ -354,13 +354,28 @@ __device__ __forceinline__ uint32_t r1_delta(uint32_t u) {
 // get T[r-1] and -- via `common`, ORed into every word at the end of the scan
 // -- all words get T[r-X] (a superset-free bound: T[r-X] is within budget
 // wherever X upper positions mismatch).
-template <int X>
+template <int X, bool CLAMP = true>
 __device__ __forceinline__ void slice_bcast(uint32_t e, uint32_t lane4, uint32_t T_s,
                                             uint32_t acc_lane_s, uint32_t& common) {
     // e = slot | r << 16, slot = (ek * 32 + eh5) * 4 | el5 << 11.  Lane L's
     // word ek is at acc + ek * 128 + 4L (the block is aligned to its size);
     // T[rho][el5][L ^ eh5] at T + rho * 4096 + el5 * 128 + 4 (L ^ eh5)
     // (radius >= 5 covers all five positions: row 6 is all ones)
+    if constexpr (!CLAMP) {
+        // r <= d <= 6: every row r, r - 1, r - X exists (r >= 2 >= X), so the
+        // three rows are one address and two immediate offsets:
+        // (e >> 4) & 0xFF80 = r * 4096 + el5 * 128
+        const uint32_t toff = T_s + ((e >> 4) & 0xFF80u) + ((e & 0x7Cu) ^ lane4);
+        const uint32_t aw = acc_lane_s | (e & 0x780u);
+        red_or(aw, lds32(toff));
+        if constexpr (X >= 1) common |= lds32(toff - (uint32_t)X * 4096u);
+        if constexpr (X >= 2) {
+            const uint32_t b = lds32(toff - 4096u);
+#pragma unroll
+            for (int u = 0; u < 3 * X; ++u) red_or(aw ^ (r1_delta<X>(6u + (uint32_t)u) * 4u), b);
+        }
+        return;
+    }
     const uint32_t r = e >> 16;
     const uint32_t toff = T_s + ((e >> 4) & 0xF80u) + ((e & 0x7Cu) ^ lane4);
     const uint32_t aw = acc_lane_s | (e & 0x780u);
@@ -387,6 +402,7 @@ struct SliceWarp {
     uint32_t vmask;          // this lane's real windows among its NWl
     uint32_t uL, hL, dword4, r1row;  // r = 1 rounds: update u of hit h
     bool r1lane;
+    bool rclamp;  // d > 6: r >= 2 broadcasts clamp their table rows (slice_bcast)
     uint32_t km[4];
     int NWl, Wp;
 };
@@ -457,6 +473,7 @@ __device__ __forceinline__ SliceWarp<S, SMEM> slice_setup(const SliceArgs& a, ui
     w.dword4 = r1_delta<X>(w.uL) * 4u;
     w.r1row = w.R1_s + w.uL * 4u;
     w.r1lane = w.lane < (uint32_t)(C::HPRA * C::NUA);
+    w.rclamp = a.dp > 6u;
     w.NWl = a.NWl;
     w.Wp = a.Wp;
     return w;
@@ -606,6 +623,22 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
                 red_or(acc | (sl & 0x7FFu), 1u << (sl >> 11));
             }
         }
+        if constexpr (C::NUB == C::NUA) {
+            // X = 2: loops (A) and (B) both take HPRA hits per round and give
+            // lane L the same hit L / NUA, so one round applies both of its
+            // updates -- one queue read and one loop step for the two reds
+            uint32_t accB = w.acc_s ^ (r1_delta<X>(6u + w.uL) * 4u);
+            asm volatile("" : "+r"(accB));
+#pragma unroll 1
+            for (uint32_t b1 = 0; b1 < t1; b1 += C::HPRA, qa1 += 2u * C::HPRA) {
+                if (b1 + w.hL < r1lim) {
+                    const uint32_t sl = lds16(qa1);
+                    PMS_CHECK(sl != kPoison16);
+                    red_or(acc_d ^ (sl & 0x7FFu), lds32(r1row + (sl >> 11) * 64u));
+                    red_or(accB ^ (sl & 0x7FFu), 1u << (sl >> 11));
+                }
+            }
+        } else {
 #pragma unroll 1
         for (uint32_t b1 = 0; b1 < t1; b1 += C::HPRA, qa1 += 2u * C::HPRA) {
             if (b1 + w.hL < r1lim) {  // (A) own word + lane flips
@@ -629,12 +662,22 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
                 }
             }
         }
+        }
         __syncwarp();
+        if (w.rclamp) {
 #pragma unroll 1
-        for (uint32_t b2 = 0; b2 < t2; ++b2) {
-            const uint32_t e = lds32(w.q2_s + 4u * b2);  // same address: broadcast
-            PMS_CHECK(e != kPoison32);
-            slice_bcast<X>(e, w.lane4, w.T_s, w.acc_lane_s, common);
+            for (uint32_t b2 = 0; b2 < t2; ++b2) {
+                const uint32_t e = lds32(w.q2_s + 4u * b2);  // same address: broadcast
+                PMS_CHECK(e != kPoison32);
+                slice_bcast<X, true>(e, w.lane4, w.T_s, w.acc_lane_s, common);
+            }
+        } else {
+#pragma unroll 1
+            for (uint32_t b2 = 0; b2 < t2; ++b2) {
+                const uint32_t e = lds32(w.q2_s + 4u * b2);
+                PMS_CHECK(e != kPoison32 && (e >> 16) <= 6u);
+                slice_bcast<X, false>(e, w.lane4, w.T_s, w.acc_lane_s, common);
+            }
         }
 #ifdef PMS_DEBUG_CHECKS
         __syncwarp();  // every lane has read its entries: poison them again
