@@ -336,6 +336,7 @@ struct pms_plan {
     SliceFn sfn = nullptr;
     SliceFn sfn_ht = nullptr;  // the same search, hand-off on the staged tables (few blocks)
     int last_ht = 0;
+    int sparse_handoff = 2;    // sparse-mode threshold (alive candidates) of the other instances
     int seqpar = 0;                 // sequence-parallel slice kernel (pms_search_slice_sp)
     uint32_t* d_spmask = nullptr;   // its per-block masks and counters
     uint32_t* d_spcnt = nullptr;
@@ -456,6 +457,22 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
             p->sfn = spf;
         }
         if (p->in_smem && !p->seqpar) p->sfn_ht = slice_ht_kernel(S, l - S);
+        // sparse mode pays per candidate what a dense scan pays per hit: its
+        // threshold follows the expected pass-1 hits per scan, W * P(prefix
+        // within d) for iid uniform bases (a tuning knob; the set is the same).
+        // Measured: (15,4) ~67 hits/scan best at 2 (155.6 us; 8: 161.8),
+        // (16,5) ~163 hits/scan best at 8-12 (1.98 ms; 2: 2.14)
+        {
+            double ph = 0.0;  // P(Binomial(LP, 1/4) >= LP - d)
+            const int LPs = l - S;
+            for (int m = std::max(0, LPs - d); m <= LPs; ++m) {
+                double c = 1.0;
+                for (int q = 0; q < m; ++q) c = c * (LPs - q) / (q + 1);
+                ph += c * std::pow(0.25, m) * std::pow(0.75, LPs - m);
+            }
+            const double hits = p->W * ph;
+            p->sparse_handoff = std::max(2, std::min(12, (int)(hits / 20.0)));
+        }
         p->G = 32; p->NW = p->NWl; p->generic = 0;
         p->block = kSliceThreadsFor(S);
         p->d_ball = ensure_slice_ball_table(p->dev);
@@ -491,7 +508,9 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
             return fail_cuda(__LINE__);
         }
         if (cudaMalloc(&p->d_table, p->tab_bytes) != cudaSuccess ||
-            cudaMalloc(&p->d_planes, p->plane_bytes) != cudaSuccess ||
+            // prefix planes [n][LP][4][32] (staged), then the suffix planes
+            // [n][S][4][32] (sparse mode, read through L1/L2)
+            cudaMalloc(&p->d_planes, (size_t)p->n * p->l * 512) != cudaSuccess ||
             cudaMalloc(&p->d_slots, p->slot_bytes) != cudaSuccess ||
             cudaMalloc(&p->d_state, sizeof(DevState)) != cudaSuccess ||
             cudaMallocHost(&p->h_state, sizeof(DevState)) != cudaSuccess ||
@@ -644,6 +663,7 @@ namespace {
 SliceArgs slice_args(const pms_plan* p) {
     SliceArgs sa{};
     sa.planes = static_cast<const uint32_t*>(p->d_planes);
+    sa.splanes = static_cast<const uint32_t*>(p->d_planes) + p->plane_bytes / 4;
     sa.slots = static_cast<const uint16_t*>(p->d_slots);
     sa.words = static_cast<const uint32_t*>(p->d_table);
     sa.ball = p->d_ball;
@@ -720,6 +740,11 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
         static const char* ht_env = std::getenv("PMS_HANDOFF_TABLES");
         const bool ht = p->sfn_ht && (ht_env ? std::atoi(ht_env) != 0 : span / kUnit < 2ull * warps);
         p->last_ht = ht ? 1 : 0;
+        // hand-off threshold: the tables check takes one candidate at a time
+        // (1, or 2 for d >= 5); sparse mode (the other instances) takes up to
+        // kSparseHandoff candidates together
+        if (p->launch.handoff <= 0) sa.handoff = ht ? (p->d >= 5 ? 2 : 1) : p->sparse_handoff;
+        if (!ht && sa.handoff > 32) sa.handoff = 32;  // one sparse list entry per lane
         int sp_words = 0, sp_blocks = 0;
         if (p->seqpar) {
             sa.spmask = p->d_spmask;
@@ -731,7 +756,7 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
         if (cudaEventRecord(p->ev[0], s) != cudaSuccess) return fail_cuda(__LINE__);
         const SlicePackFn pack = slice_pack_kernel(p->S);
         const unsigned pack_y =
-            (unsigned)((p->Wp + p->LP * 128 + kSlicePackThreads - 1) / kSlicePackThreads);
+            (unsigned)((p->Wp + p->l * 128 + kSlicePackThreads - 1) / kSlicePackThreads);
         pack<<<dim3((unsigned)p->n, pack_y), kSlicePackThreads, 0, s>>>(
             d_seqs, p->n, p->t, p->l, p->W, p->NWl, p->LP, static_cast<uint32_t*>(p->d_planes),
             static_cast<uint16_t*>(p->d_slots), static_cast<uint32_t*>(p->d_table), p->d_state,

@@ -51,6 +51,7 @@ namespace pms {
 
 struct SliceArgs {
     const uint32_t* planes;   // [n][LP][4][32] match planes (global)
+    const uint32_t* splanes;  // [n][S][4][32] match planes of the suffix positions (sparse mode)
     const uint16_t* slots;    // [n][Wp] r = 0 slot of each window (global)
     const uint32_t* words;    // [n][Wp] packed Bp32 windows (hand-off checks, global)
     const uint32_t* ball;     // slice ball table (kSTWords words, global)
@@ -230,14 +231,17 @@ __global__ void __launch_bounds__(kSlicePackThreads) pms_pack_slice(
         // (word = k * 32 + lane, word-major; < 2 KB at S <= 7) | bit << 11
         slots[(long long)i * Wp + k] =
             (uint16_t)(k < W ? (((kw * 32u + (eH & 31u)) * 4u) | ((eL & 31u) << 11)) : 0u);
-    } else if (item < Wp + LP * 128) {
+    } else if (item < Wp + l * 128) {
+        // positions j < LP: the staged prefix planes; j >= LP: the suffix
+        // planes [n][S][4][32] after all prefix planes (sparse mode)
         const int idx = item - Wp;
         const int j = idx >> 7, b = (idx >> 5) & 3, ln = idx & 31;
         uint32_t v = 0;
         const int k0 = ln * NWl, nq = min(NWl, W - k0);
         for (int q = 0; q < nq; ++q)
             if (code[k0 + q + j] == (uint8_t)b) v |= 1u << q;
-        planes[(long long)i * LP * 128 + idx] = v;
+        if (j < LP) planes[(long long)i * LP * 128 + idx] = v;
+        else planes[(long long)n * LP * 128 + (long long)i * S * 128 + (idx - LP * 128)] = v;
     }
 }
 
@@ -795,6 +799,131 @@ __device__ __forceinline__ bool slice_check_one(const SliceWarp<S, SMEM>& w, con
     return true;
 }
 
+// Sparse mode (the hand-off of the throughput instances): once
+// at most a.handoff candidates of the block are alive, the remaining
+// sequences are tested per candidate -- still per candidate and in input
+// order (PAPER.md:63's skip rule), on the bit-sliced planes of all l
+// positions: the block's prefix count (one pass 1 shared by the candidates,
+// K + prefix matches, as slice_pass1) plus the candidate's own suffix match
+// planes (global, L1/L2), so a window matches iff K + prefix + suffix
+// matches >= 16 + S, i.e. at most d mismatches over all l positions -- for a
+// lane's windows at once, no per-window or per-hit work.  The candidates'
+// suffix codes are listed in the warp's word block (zero between scans), which
+// is cleared again before the next block.
+template <int N>
+__device__ __forceinline__ void slice_count3(const uint32_t (&m)[N], uint32_t& s0, uint32_t& s1,
+                                             uint32_t& s2) {
+    static_assert(N >= 3 && N <= 7, "suffix digits");
+    constexpr int N1 = N / 2, N2 = N1 / 2;
+    uint32_t v0[N], y0[N1];
+#pragma unroll
+    for (int j = 0; j < N; ++j) v0[j] = m[j];
+    s0 = csa_col<N>(v0, y0);
+    uint32_t y1[N2 > 0 ? N2 : 1];
+    s1 = csa_col<N1>(y0, y1);
+    s2 = N2 > 0 ? y1[0] : 0u;
+}
+
+template <int S, int LP, bool SMEM>
+__device__ __forceinline__ void slice_sparse(const SliceWarp<S, SMEM>& w, const SliceArgs& a,
+                                             const uint32_t (&po)[LP], int i0,
+                                             const uint32_t (&alive)[SliceCfg<S>::KW],
+                                             unsigned long long cbase, unsigned long long& scanned) {
+    constexpr int KW = SliceCfg<S>::KW;
+    constexpr uint32_t kGe = 16u + (uint32_t)S;  // K + matches >= 16 + S <=> <= d mismatches
+    const uint32_t lane = w.lane;
+    const uint32_t L_s = w.acc_s;  // the list (the word block is zero here)
+    uint32_t A = 0;                 // warp-uniform
+#pragma unroll
+    for (int k = 0; k < KW; ++k) {
+        uint32_t hold = __ballot_sync(kFull, alive[k] != 0u);
+        while (hold) {
+            const int src = __ffs(hold) - 1;
+            hold &= hold - 1;
+            uint32_t bits = __shfl_sync(kFull, alive[k], src);
+            while (bits) {
+                const uint32_t b = (uint32_t)__ffs(bits) - 1u;
+                bits &= bits - 1;
+                PMS_CHECK(A < 32u);
+                if (lane == 0) sts32(L_s + 4u * A, blk_sfx<Bp32, S>((uint32_t)src, (uint32_t)k, b));
+                ++A;
+            }
+        }
+    }
+    __syncwarp();
+    const uint32_t A0 = A;
+    int i = i0;
+    for (; i < a.n && A; ++i) {
+        uint32_t m[LP], c[5];
+        if constexpr (SMEM) {
+            const uint32_t P = w.planes_s + (uint32_t)i * (uint32_t)(LP * 512);
+#pragma unroll
+            for (int j = 0; j < LP; ++j) m[j] = lds32(P + po[j]);
+        } else {
+            const char* P = reinterpret_cast<const char*>(w.planes) + (size_t)i * (LP * 512);
+#pragma unroll
+            for (int j = 0; j < LP; ++j) m[j] = __ldg(reinterpret_cast<const uint32_t*>(P + po[j]));
+        }
+        slice_count<LP>(m, w.km, c);
+        const uint32_t* sp = a.splanes + (size_t)i * (S * 128) + lane;
+        // does the candidate with suffix code x have a window within d here?
+        // (t = c + suffix matches, five planes, no overflow: K + l <= 31;
+        // t >= 16 + S bit-sliced from the low bit up)
+        auto test = [&](const uint32_t (&sm)[S]) -> uint32_t {
+            uint32_t s0, s1, s2;
+            slice_count3<S>(sm, s0, s1, s2);
+            const uint32_t t0 = c[0] ^ s0;
+            uint32_t k = c[0] & s0;
+            const uint32_t t1 = c[1] ^ s1 ^ k;
+            k = (c[1] & s1) | (k & (c[1] ^ s1));
+            const uint32_t t2 = c[2] ^ s2 ^ k;
+            k = (c[2] & s2) | (k & (c[2] ^ s2));
+            const uint32_t t3 = c[3] ^ k;
+            k = c[3] & k;
+            const uint32_t t4 = c[4] | k;
+            const uint32_t t[5] = {t0, t1, t2, t3, t4};
+            uint32_t g = kFull;
+#pragma unroll
+            for (int b = 0; b < 5; ++b) g = ((kGe >> b) & 1u) ? (t[b] & g) : (t[b] | g);
+            return g & w.vmask;
+        };
+        uint32_t keep = 0;
+        // (two candidates per step, their loads overlapped, measured slower:
+        // (15,4) +4 %, (16,5) +1 %)
+#pragma unroll 1
+        for (uint32_t j = 0; j < A; ++j) {
+            const uint32_t x = lds32(L_s + 4u * j);  // broadcast
+            uint32_t sm[S];
+#pragma unroll
+            for (int q = 0; q < S; ++q)
+                sm[q] = __ldg(sp + (q * 4 + ((x >> (2 * (S - 1 - q))) & 3u)) * 32u);
+            keep |= (uint32_t)__any_sync(kFull, test(sm) != 0u) << j;
+        }
+        scanned += A;
+        // drop the candidates with no window within d in sequence i
+        const uint32_t x = lane < A ? lds32(L_s + 4u * lane) : 0u;
+        __syncwarp();
+        if (lane < A && ((keep >> lane) & 1u)) sts32(L_s + 4u * (uint32_t)__popc(keep & ((1u << lane) - 1u)), x);
+        __syncwarp();
+        A = (uint32_t)__popc(keep);
+    }
+    if (A) {  // survivors of all n sequences
+        PMS_CHECK(i == a.n);
+        const uint32_t x = lane < A ? lds32(L_s + 4u * lane) : 0u;
+        unsigned long long slot = 0;
+        if (lane == 0) slot = atomicAdd(a.nout, (unsigned long long)A);
+        slot = __shfl_sync(kFull, slot, 0) + lane;
+        if (lane < A && slot < a.cap) {
+            const unsigned long long code = cbase + x;
+            if (a.out_wide) static_cast<unsigned long long*>(a.out)[slot] = code;
+            else static_cast<uint32_t*>(a.out)[slot] = (uint32_t)code;
+        }
+    }
+    __syncwarp();
+    if (lane < A0) sts32(L_s + 4u * lane, 0u);  // the word block is zero again
+    __syncwarp();
+}
+
 template <int S, int LP, bool SMEM, bool HT = false>
 __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs a) {
     using B = BlkTraits<S>;
@@ -892,6 +1021,10 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
                         }
                     }
                 }
+                continue;
+            }
+            if constexpr (!HT) {  // throughput instances: sparse mode
+                slice_sparse<S, LP, SMEM>(w, a, po, i, alive, cbase, scanned);
                 continue;
             }
             // at most a.handoff survivors: the whole warp finishes each one from

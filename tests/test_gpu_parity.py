@@ -636,11 +636,13 @@ print("ok")
 @pytest.mark.parametrize("force", ["0", "1"])
 @pytest.mark.parametrize("cfg", [1, 2, 3])
 def test_handoff_check_kinds(cfg, force):
-    """The slice family's two hand-off checks -- on the staged
-    planes and slots (chosen for ranges with few blocks per warp) and on the
-    packed words -- each forced in a fresh process (PMS_HANDOFF_TABLES is read
-    once), give the golden set of (11,3), (13,3) and (15,4); mode_flags bit 1
-    reports the kind that ran.  With the default, (13,3) (4,096 blocks for
+    """The slice family's two hand-off paths -- the check on
+    the staged planes and slots, one candidate at a time (chosen for ranges
+    with few blocks per warp), and the sparse mode (candidate lists of up to
+    32 entries tested on the planes of all l positions) -- each forced in a
+    fresh process (PMS_HANDOFF_TABLES is read once), give the golden set of
+    (11,3), (13,3) and (15,4), whole and on a sub-range, for hand-off
+    thresholds 1..5000; mode_flags bit 1 reports the kind that ran.  With the default, (13,3) (4,096 blocks for
     4,736 warps) runs the tables check and (15,4) the packed-word one."""
     import subprocess
     import sys
@@ -659,6 +661,11 @@ lo, hi = 4 ** g["l"] // 3, 4 ** g["l"] // 3 + 3 * 4 ** (g["l"] - 3) + 777
 r = pms.find_ex(s, g["l"], g["d"], lo=lo, hi=hi)
 want = [c for c in g["codes"] if lo <= c < hi]
 assert r.status == 0 and r.codes.tolist() == want
+for h in (1, 2, 8, 31, 32, 5000):  # sparse-mode / tables-check thresholds (32: one entry per lane)
+    r = pms.find_ex(s, g["l"], g["d"], launch=pms.Launch(handoff=h))
+    assert r.status == 0 and r.codes.tolist() == g["codes"], h
+    r = pms.find_ex(s, g["l"], g["d"], lo=lo, hi=hi, launch=pms.Launch(handoff=h))
+    assert r.status == 0 and r.codes.tolist() == want, h
 print("ok")
 """
     p = subprocess.run([sys.executable, "-c", code],

@@ -284,3 +284,42 @@ def test_overlap_prepass_plan_parity(orc):
                 got = sorted(out[:int(cnt.item())].cpu().numpy().astype(np.uint32).tolist())
                 assert got == want
                 assert (st.pack_ms == 0.0) == bool(ov) and st.search_ms > 0.0
+
+
+def test_slice_sparse_mode_dense_and_ranges(orc):
+    """The sparse mode (packed-word instances, PMS_HANDOFF_TABLES=0, fresh
+    process) on small random instances: dense hits, every block size, d from
+    0 to LP - 1, unaligned ranges, thresholds 1..32 -- each set equal to the
+    oracle's."""
+    import subprocess
+    import sys
+    cases = []
+    rng = random.Random(7)
+    for S in (5, 6, 7):
+        for l in (S + 2, S + 4, 16):
+            d = rng.randint(0, l - S - 1)
+            s = fmgen.random_sequences(5, 120, 77 * S + l)
+            lo = rng.randrange(0, 4 ** l - 300000) if l > 9 else 0
+            hi = lo + 300000 if l > 9 else 4 ** l
+            want = orc.find(s, l, d, lo=lo, hi=hi).codes.tolist()
+            cases.append((s.tolist(), l, d, S, lo, hi, want))
+    code = f"""
+import json, sys
+import numpy as np
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import paper_1403_1313_b200 as pms
+cases = json.loads(sys.stdin.read())
+for s, l, d, S, lo, hi, want in cases:
+    s = np.array(s, dtype=np.uint8)
+    for h in (1, 3, 8, 32):
+        r = pms.find_ex(s, l, d, lo=lo, hi=hi,
+                        launch=pms.Launch(algo=pms.ALGO_SLICE, block_digits=S, handoff=h))
+        assert r.status == 0 and r.stats.algo == pms.ALGO_SLICE, (l, d, S, h, r.status)
+        assert (r.stats.mode_flags >> 1) & 1 == 0
+        assert r.codes.tolist() == want, (l, d, S, h)
+print("ok")
+"""
+    p = subprocess.run([sys.executable, "-c", code], input=json.dumps(cases),
+                       env={**os.environ, "PMS_HANDOFF_TABLES": "0"},
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stderr[-2000:]
