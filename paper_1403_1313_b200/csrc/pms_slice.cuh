@@ -1023,39 +1023,33 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
                 }
                 continue;
             }
-            if constexpr (!HT) {  // throughput instances: sparse mode
+            if constexpr (!HT) {
+                // throughput instances: sparse mode (the list of at most
+                // a.handoff candidates, all remaining sequences)
                 slice_sparse<S, LP, SMEM>(w, a, po, i, alive, cbase, scanned);
                 continue;
-            }
-            // at most a.handoff survivors: the whole warp finishes each one from
-            // sequence i with the per-candidate check (packed words, L1/L2)
-            for (;;) {
-                uint32_t pick = kFull;
+            } else {
+                // latency instances: at most a.handoff survivors, each finished
+                // from sequence i by the whole warp on the staged tables (a lone
+                // warp's chain is the run time here; no L2 round trips)
+                for (;;) {
+                    uint32_t pick = kFull;
 #pragma unroll
-                for (int k = KW - 1; k >= 0; --k)
-                    if (alive[k]) pick = ((uint32_t)k << 5) | (__ffs(alive[k]) - 1);
-                const uint32_t holder = __ballot_sync(kFull, pick != kFull);
-                if (!holder) break;
-                const int src = __ffs(holder) - 1;
-                const uint32_t pk = __shfl_sync(kFull, pick, src);
-                const uint32_t k = pk >> 5;
-                if ((int)lane == src) {
+                    for (int k = KW - 1; k >= 0; --k)
+                        if (alive[k]) pick = ((uint32_t)k << 5) | (__ffs(alive[k]) - 1);
+                    const uint32_t holder = __ballot_sync(kFull, pick != kFull);
+                    if (!holder) break;
+                    const int src = __ffs(holder) - 1;
+                    const uint32_t pk = __shfl_sync(kFull, pick, src);
+                    const uint32_t k = pk >> 5;
+                    if ((int)lane == src) {
 #pragma unroll
-                    for (int q = 0; q < KW; ++q)
-                        if (q == (int)k) alive[q] &= alive[q] - 1;
-                }
-                const unsigned long long code = cbase + blk_sfx<Bp32, S>(src, k, pk & 31u);
-                // HT (few blocks per warp: latency-bound, a lone warp's chain is
-                // the run time): the check on the staged tables; else the packed
-                // words (fewer instructions, L2 latency hidden by other warps)
-                bool ok;
-                if constexpr (HT)
-                    ok = slice_check_one<S, LP, SMEM>(w, po, i, a.n, k, (uint32_t)src, pk & 31u, scanned);
-                else
-                    ok = check_sequences<Bp32>(a.words, i, a.n, a.Wp, Bp32::prep(code), a.dp, (int)lane,
-                                               scanned);
-                if (ok) {
-                    if (lane == 0) {
+                        for (int q = 0; q < KW; ++q)
+                            if (q == (int)k) alive[q] &= alive[q] - 1;
+                    }
+                    const unsigned long long code = cbase + blk_sfx<Bp32, S>(src, k, pk & 31u);
+                    if (slice_check_one<S, LP, SMEM>(w, po, i, a.n, k, (uint32_t)src, pk & 31u, scanned) &&
+                        lane == 0) {
                         const unsigned long long slot = atomicAdd(a.nout, 1ull);
                         if (slot < a.cap) {
                             if (a.out_wide) static_cast<unsigned long long*>(a.out)[slot] = code;
