@@ -11,8 +11,17 @@ LIB_RELEASE = os.path.join(PKG, "libpms_b200.so")
 LIB_DEBUG = os.path.join(PKG, "libpms_b200_debug.so")  # -DPMS_DEBUG_CHECKS (bounds counters)
 # PMS_DEBUG_LIB=1 selects the bounds-checked build for this process
 LIB = LIB_DEBUG if os.environ.get("PMS_DEBUG_LIB") == "1" else LIB_RELEASE
-# PMS_LIB_OVERRIDE=/path/lib.so loads a variant build (tuning experiments, scripts/variants.py)
-LIB = os.environ.get("PMS_LIB_OVERRIDE") or LIB
+# PMS_LIB_OVERRIDE=build/variants/NAME/libpms_b200.so loads a variant build of
+# this source tree (tuning experiments, scripts/variants.py); nothing else is
+# accepted
+VARIANTS = os.path.join(ROOT, "build", "variants")
+_ovr = os.environ.get("PMS_LIB_OVERRIDE")
+if _ovr:
+    _real = os.path.realpath(_ovr)
+    if not (_real.startswith(os.path.realpath(VARIANTS) + os.sep) and
+            os.path.basename(_real) == "libpms_b200.so"):
+        raise RuntimeError(f"PMS_LIB_OVERRIDE must name build/variants/*/libpms_b200.so, got {_ovr!r}")
+    LIB = _real
 # pms.cu: 32-bit-word kernels + host code; pms64.cu: 64-bit-word kernels (l <= 31);
 # pms_slice.cu / pms_roof.cu: the slice family's kernels and roofline kernels
 SOURCES = [os.path.join(CSRC, f) for f in ("pms.cu", "pms64.cu", "pms_slice.cu",

@@ -1323,7 +1323,8 @@ extern "C" int64_t pms_debug_violations(int32_t reset) {
     }
     int64_t total = (int64_t)v;
     for (int64_t x : {pms::debug_violations64(reset), pms::debug_violations_slice(reset),
-                      pms::debug_violations_roof(reset)}) {  // the other TUs' counters
+                      pms::debug_violations_roof(reset),
+                      pms::debug_violations_ht(reset)}) {  // the other TUs' counters
         if (x < 0) return x;
         total += x;
     }

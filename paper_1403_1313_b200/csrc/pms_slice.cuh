@@ -95,6 +95,7 @@ SlicePackFn slice_pack_kernel(int S);                      // pms_slice.cu
 SliceRoofFn slice_roofline_kernel(int S, int LP, int mode, bool smem);  // pms_roof.cu
 int64_t debug_violations_slice(int reset);
 int64_t debug_violations_roof(int reset);
+int64_t debug_violations_ht(int reset);
 
 // Slice ball table: T[rho][e][m] (rho = 0..6, as pms_search_block's) then the
 // radius-1 rows R1[e][u] (16 words per e): u = 0: T[1][e][0]; u = 1..5:

@@ -36,6 +36,21 @@ SliceFn slice_ht_kernel(int S, int LP) {
     return nullptr;
 }
 
+int64_t debug_violations_ht(int reset) {
+#ifdef PMS_DEBUG_CHECKS
+    unsigned int v = 0;
+    if (cudaMemcpyFromSymbol(&v, g_pms_violations, sizeof(v)) != cudaSuccess) return -2;
+    if (reset) {
+        const unsigned int z = 0;
+        cudaMemcpyToSymbol(g_pms_violations, &z, sizeof(z));
+    }
+    return (int64_t)v;
+#else
+    (void)reset;
+    return 0;
+#endif
+}
+
 }  // namespace pms
 
 #ifdef PMS_TRACE
