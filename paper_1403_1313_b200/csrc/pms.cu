@@ -254,7 +254,7 @@ const uint32_t* ensure_ball_table(int dev) {
 }
 
 // The slice family's ball table (pms_slice.cuh): the rows of T, then the
-// 16-word radius-1 rows R1[e][u].  Once per device, like g_ball.
+// radius-1 rows R1[e][u] (kSR1Stride words apart).  Once per device, like g_ball.
 uint32_t* g_sball[64] = {nullptr};
 
 const uint32_t* ensure_slice_ball_table(int dev) {
@@ -271,7 +271,7 @@ const uint32_t* ensure_slice_ball_table(int dev) {
             h[idx] = w;
         }
         for (int e = 0; e < 32; ++e) {
-            uint32_t* r = &h[kSR1Off + e * 16];
+            uint32_t* r = &h[kSR1Off + e * kSR1Stride];
             r[0] = h[1024 + e * 32 + 0];
             for (int q = 0; q < 5; ++q) r[1 + q] = h[1024 + e * 32 + (1 << q)];
             for (int u = 6; u < 15; ++u) r[u] = 1u << e;

@@ -98,11 +98,15 @@ int64_t debug_violations_roof(int reset);
 int64_t debug_violations_ht(int reset);
 
 // Slice ball table: T[rho][e][m] (rho = 0..6, as pms_search_block's) then the
-// radius-1 rows R1[e][u] (16 words per e): u = 0: T[1][e][0]; u = 1..5:
+// radius-1 rows R1[e][u] (kSR1Stride words per e): u = 0: T[1][e][0]; u = 1..5:
 // T[1][e][1 << (u-1)]; u = 6..14: 1 << e (the centre bit, for the words one
 // upper position away); 15: 0.
 constexpr int kSR1Off = 7 * 1024;
-constexpr int kSTWords = kSR1Off + 32 * 16;  // 30 KB
+// R1 rows padded to 17 words: the rows of the 5 hits of an r = 1 round then
+// start in 5 different banks (a 16-word stride put them all in 2: ~2.8-way
+// conflicts on the row loads, ncu source page)
+constexpr int kSR1Stride = 17;
+constexpr int kSTWords = kSR1Off + 32 * kSR1Stride;  // 30.1 KB
 constexpr int kSliceMaxLP = 11;              // l <= 16, S >= 5
 #ifndef PMS_SLICE_R0_DIRECT
 #define PMS_SLICE_R0_DIRECT 1  // r = 0 hits resolved per lane (no queue); 0: queued
@@ -570,7 +574,7 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
             r1m ^= 1u << q;
             const uint32_t sl = slot_of(q);
             const uint32_t base = acc | (sl & 0x7FFu);
-            const uint32_t row = w.R1_s + (sl >> 11) * 64u;
+            const uint32_t row = w.R1_s + (sl >> 11) * (4u * kSR1Stride);
 #pragma unroll
             for (int u = 0; u < NU; ++u)
                 red_or(base ^ (r1_delta<X>((uint32_t)u) * 4u), lds32(row + (uint32_t)u * 4u));
@@ -639,7 +643,7 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
                 if (b1 + w.hL < r1lim) {
                     const uint32_t sl = lds16(qa1);
                     PMS_CHECK(sl != kPoison16);
-                    red_or(acc_d ^ (sl & 0x7FFu), lds32(r1row + (sl >> 11) * 64u));
+                    red_or(acc_d ^ (sl & 0x7FFu), lds32(r1row + (sl >> 11) * (4u * kSR1Stride)));
                     red_or(accB ^ (sl & 0x7FFu), 1u << (sl >> 11));
                 }
             }
@@ -650,7 +654,7 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
                 const uint32_t sl = lds16(qa1);
                 PMS_CHECK(sl != kPoison16);
                 // (acc | off) ^ d == (acc ^ d) | off: d and off lie inside the block
-                red_or(acc_d ^ (sl & 0x7FFu), lds32(r1row + (sl >> 11) * 64u));
+                red_or(acc_d ^ (sl & 0x7FFu), lds32(r1row + (sl >> 11) * (4u * kSR1Stride)));
             }
         }
         if constexpr (X >= 1) {  // (B) the words one upper position away: centre bit
@@ -706,7 +710,7 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
 #pragma unroll
             for (int u = 0; u < NU; ++u)
                 red_or(base ^ (r1_delta<X>((uint32_t)u) * 4u),
-                       lds32(w.R1_s + ((sl >> 11) * 16u + (uint32_t)u) * 4u));
+                       lds32(w.R1_s + ((sl >> 11) * (uint32_t)kSR1Stride + (uint32_t)u) * 4u));
         }
         while (__any_sync(kFull, r2m != 0u)) {
             uint32_t rec = kFull;
