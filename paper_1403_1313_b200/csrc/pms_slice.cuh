@@ -23,14 +23,14 @@
 //   cycles per warp instruction whatever the number of active lanes
 //   (tests/tools/ubench_smem.cu), so hits are resolved full-width instead of
 //   by divergent per-lane loops:
-//   * r = 0 hits (the window's own suffix only) and r = 1 hits (the radius-1
-//     ball, 6 + 3X words) are appended, as precomputed 12-bit slots
-//     (word * 32 + bit of the window's suffix in the block's mask), to two
-//     per-warp queues; one shared atomicAdd claims both queue positions;
-//   * r = 0 queue: 32 hits per atomic instruction;
-//   * r = 1 queue: lane L applies update u = L mod NU of hit L / NU (NU =
-//     6 + 3X words per ball; 3 hits per instruction at S = 6): word
-//     slot/32 XOR a per-lane constant, bits from a 16-entry row per e;
+//   * r = 0 hits (the window's own suffix only) are resolved by the lane
+//     that found them: one slot load and one red each;
+//   * r = 1 hits (the radius-1 ball, NU = 6 + 3X words) are appended, as
+//     precomputed slots (byte offset of the window's suffix word in the
+//     block's mask | bit << 11), to a per-warp queue (one shared atomicAdd
+//     claims the positions of all hit classes) and resolved hit-major: lane
+//     L takes hit b + L and applies its NU updates, word = slot XOR a
+//     compile-time constant, bits from the hit's padded R1 row;
 //   * r >= 2 hits (rare): broadcast to all lanes, which read their own words'
 //     bits from the ball table T[r][e][m] (as pms_search_block).
 //   A queue overflow (possible only when hits are dense: small LP, large d)
@@ -129,11 +129,6 @@ struct SliceCfg {
     static constexpr int X = S - 5;
     static constexpr int KW = 1 << (2 * X);   // mask words per lane
     static constexpr int NU = 6 + 3 * X;      // words of a radius-1 ball
-    // r = 1 rounds in two loops: (A) the own word + the 5 lane flips (R1 row
-    // bits), 5 hits per round; (B) the 3X words one upper position away (the
-    // centre bit, no table load), 32 / 3X hits per round
-    static constexpr int NUA = 6, HPRA = 32 / NUA;
-    static constexpr int NUB = 3 * X, HPRB = NUB ? 32 / NUB : 0;
 #ifndef PMS_SLICE7_NT
 #define PMS_SLICE7_NT 1024
 #endif
@@ -409,8 +404,6 @@ struct SliceWarp {
     const uint32_t* planes;  // shared (SMEM) or global
     const uint16_t* gslots;  // global slots (!SMEM)
     uint32_t vmask;          // this lane's real windows among its NWl
-    uint32_t uL, hL, dword4, r1row;  // r = 1 rounds: update u of hit h
-    bool r1lane;
     bool rclamp;  // d > 6: r >= 2 broadcasts clamp their table rows (slice_bcast)
     uint32_t km[4];
     int NWl, Wp;
@@ -477,11 +470,6 @@ __device__ __forceinline__ SliceWarp<S, SMEM> slice_setup(const SliceArgs& a, ui
     for (int b = 0; b < 4; ++b) w.km[b] = a.kmask[b];
     const int nvalid = min(a.NWl, max(0, a.W - (int)w.lane * a.NWl));
     w.vmask = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
-    w.uL = w.lane % C::NUA;
-    w.hL = w.lane / C::NUA;
-    w.dword4 = r1_delta<X>(w.uL) * 4u;
-    w.r1row = w.R1_s + w.uL * 4u;
-    w.r1lane = w.lane < (uint32_t)(C::HPRA * C::NUA);
     w.rclamp = a.dp > 6u;
     w.NWl = a.NWl;
     w.Wp = a.Wp;
@@ -617,13 +605,11 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
         if (lane == 0) sts32(w.qc_s, 0u);  // claims are done; next use after __syncwarp
         // loop-invariant shared-window addresses, pinned in registers: under the
         // 64-register cap the compiler otherwise re-derives them every round
-        uint32_t acc = w.acc_s, qa0 = w.q0_s + 2u * lane, qa1 = w.q1_s + 2u * w.hL;
-        uint32_t r1row = w.r1row, acc_d = w.acc_s ^ w.dword4;
-        asm volatile("" : "+r"(acc), "+r"(qa0), "+r"(qa1), "+r"(r1row), "+r"(acc_d));
+        uint32_t acc = w.acc_s, qa0 = w.q0_s + 2u * lane;
+        asm volatile("" : "+r"(acc), "+r"(qa0));
         // round loops with warp-uniform trip counts and predicated bodies: a
         // lane-dependent trip count let the warp run on diverged into the
         // broadcasts and the end of scan, executing both twice (measured)
-        const uint32_t r1lim = w.r1lane ? t1 : 0u;
 #pragma unroll 1
         for (uint32_t b0 = 0; b0 < t0; b0 += 32u, qa0 += 64u) {
             if (b0 + lane < t0) {
@@ -632,45 +618,31 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
                 red_or(acc | (sl & 0x7FFu), 1u << (sl >> 11));
             }
         }
-        if constexpr (C::NUB == C::NUA) {
-            // X = 2: loops (A) and (B) both take HPRA hits per round and give
-            // lane L the same hit L / NUA, so one round applies both of its
-            // updates -- one queue read and one loop step for the two reds
-            uint32_t accB = w.acc_s ^ (r1_delta<X>(6u + w.uL) * 4u);
-            asm volatile("" : "+r"(accB));
+        // hit-major rounds: lane L takes hit b + L and applies all NU updates of
+        // its radius-1 ball, one red per update (the own word + 5 lane flips,
+        // bits from its padded R1 row; the 3X upper words, centre bit).  Each
+        // red instruction then touches one word per hit: few bank conflicts
+        // (packing 6 updates of one hit into one instruction put the 3X upper
+        // words of a hit -- same lane, same bank -- in one ~7-wavefront red),
+        // and no per-lane update decode
+        if (t1) {
+            uint32_t qh = w.q1_s + 2u * lane;
+            asm volatile("" : "+r"(qh));
 #pragma unroll 1
-            for (uint32_t b1 = 0; b1 < t1; b1 += C::HPRA, qa1 += 2u * C::HPRA) {
-                if (b1 + w.hL < r1lim) {
-                    const uint32_t sl = lds16(qa1);
+            for (uint32_t b1 = 0; b1 < t1; b1 += 32u, qh += 64u) {
+                if (b1 + lane < t1) {
+                    const uint32_t sl = lds16(qh);
                     PMS_CHECK(sl != kPoison16);
-                    red_or(acc_d ^ (sl & 0x7FFu), lds32(r1row + (sl >> 11) * (4u * kSR1Stride)));
-                    red_or(accB ^ (sl & 0x7FFu), 1u << (sl >> 11));
+                    const uint32_t base = acc | (sl & 0x7FFu), e5 = sl >> 11;
+                    const uint32_t row = w.R1_s + e5 * (4u * kSR1Stride);
+#pragma unroll
+                    for (int u = 0; u < 6; ++u)
+                        red_or(base ^ (r1_delta<X>((uint32_t)u) * 4u), lds32(row + 4u * (uint32_t)u));
+                    const uint32_t cb = 1u << e5;
+#pragma unroll
+                    for (int u = 6; u < C::NU; ++u) red_or(base ^ (r1_delta<X>((uint32_t)u) * 4u), cb);
                 }
             }
-        } else {
-#pragma unroll 1
-        for (uint32_t b1 = 0; b1 < t1; b1 += C::HPRA, qa1 += 2u * C::HPRA) {
-            if (b1 + w.hL < r1lim) {  // (A) own word + lane flips
-                const uint32_t sl = lds16(qa1);
-                PMS_CHECK(sl != kPoison16);
-                // (acc | off) ^ d == (acc ^ d) | off: d and off lie inside the block
-                red_or(acc_d ^ (sl & 0x7FFu), lds32(r1row + (sl >> 11) * (4u * kSR1Stride)));
-            }
-        }
-        if constexpr (X >= 1) {  // (B) the words one upper position away: centre bit
-            const uint32_t uB = lane % C::NUB, hB = lane / C::NUB;
-            uint32_t accB = w.acc_s ^ (r1_delta<X>(6u + uB) * 4u), qb = w.q1_s + 2u * hB;
-            asm volatile("" : "+r"(accB), "+r"(qb));
-            const uint32_t limB = lane < (uint32_t)(C::HPRB * C::NUB) ? t1 : 0u;
-#pragma unroll 1
-            for (uint32_t b1 = 0; b1 < t1; b1 += C::HPRB, qb += 2u * C::HPRB) {
-                if (b1 + hB < limB) {
-                    const uint32_t sl = lds16(qb);
-                    PMS_CHECK(sl != kPoison16);
-                    red_or(accB ^ (sl & 0x7FFu), 1u << (sl >> 11));
-                }
-            }
-        }
         }
         __syncwarp();
         if (w.rclamp) {
