@@ -416,7 +416,7 @@ template <int S, bool SMEM>
 __device__ __forceinline__ SliceWarp<S, SMEM> slice_setup(const SliceArgs& a, uint32_t* sdyn,
                                                          uint64_t* bar, uint32_t* qcnts) {
     using C = SliceCfg<S>;
-    constexpr int X = C::X, KW = C::KW;
+    constexpr int KW = C::KW;
     SliceWarp<S, SMEM> w;
     w.lane = threadIdx.x & 31u;
     const uint32_t wid = threadIdx.x >> 5;
@@ -575,7 +575,8 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
     const uint32_t tot = __reduce_add_sync(kFull, n012);
     const uint32_t t0 = tot & 1023u, t1 = (tot >> 10) & 1023u, t2 = tot >> 20;
     if (t0 <= (uint32_t)C::kCap0 && t1 <= (uint32_t)C::kCap1 && t2 <= (uint32_t)C::kCap2) {
-        // queue the hits (one atomic claims all three queue positions), then
+        // queue the hits (one atomic claims all three queue positions; a
+        // 5-step shuffle prefix sum instead measured +16 % at (15,4)), then
         // resolve them full-width
         if (n012) {
             const uint32_t pos = atom_add(w.qc_s, n012);
