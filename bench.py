@@ -208,40 +208,58 @@ def run_reference(args) -> int:
 
 # --------------------------------------------------------------- GPU arm
 def roofline_object(pms, plan, st, search_ms: float, clk: dict, sms: int) -> dict:
-    """Roofline of the timed kernel (DESIGN.md section 6c).
+    """Roofline of the timed kernel (DESIGN.md section 6).
 
-    achieved: the window tests of the kernel's block scans per launch
-    (block_scans x W) / mean search-kernel event time -- the hand-off's
-    per-candidate checks are left out of the numerator (cheaper per window
-    than a block scan) while their time stays in the denominator, so the
-    fraction is conservative.
-    peak (headline): R_scan, pms_plan_roofline mode 1 -- the kernel's own
-    per-scan instruction sequence at this instance's hit mix with every
-    dynamic part removed, on all SMs, measured in this run.  Also: R_pass1
-    (mode 0, the prefix test alone) and the issue roofline (warp
-    instructions per block scan from the committed ncu capture x this
-    launch's scans / 4 warp-instructions/clk/SM x SMs x the sampled clock)."""
-    achieved = st.block_scans * (plan.t - plan.l + 1) / (search_ms * 1e-3)
-    obj = {"bound": "alu", "unit": "G window-tests/s", "achieved": achieved / 1e9,
-           "achieved_basis": "block-scan window tests per launch (block_scans x W) / mean "
-                             "search-kernel event time; the hand-off's per-candidate checks "
-                             "are not counted but their time is (conservative)",
-           "executed_incl_handoff": st.issued_compares / (search_ms * 1e-3) / 1e9}
+    The kernel's work per launch is two kinds of unit (PAPER.md:63's window
+    test, done two ways): dense (block, sequence) scans -- W window tests
+    against a block's shared prefix, hits resolved as Hamming balls -- and
+    sparse-mode steps -- a short list of candidates each tested against W
+    windows.  Each kind has a measured microbenchmark of the kernel's own code
+    for that unit on this instance's tables, all SMs, same run:
+    R_scan (pms_plan_roofline mode 1) and R_sparse (mode 2).  The ideal time
+    is scans / R_scan + steps / R_sparse; frac = ideal / measured kernel time
+    (what the dynamic parts -- work counter, skip rule, list extraction,
+    load balance, tail -- cost).  achieved = executed window tests (W per scan
+    and per candidate check, pms_stats.issued_compares) / kernel time; peak =
+    the same tests / the ideal time.  Also reported: R_pass1 (mode 0, the
+    prefix test alone) with frac_vs_pass1 = dense-scan tests / R_pass1, and
+    the hardware issue roofline (ncu warp instructions of this launch / 4
+    warp-instructions/clk/SM x SMs x the sampled clock)."""
+    W = plan.t - plan.l + 1
+    t = search_ms * 1e-3
+    tests = st.issued_compares
+    obj = {"bound": "alu", "unit": "G window-tests/s", "achieved": tests / t / 1e9,
+           "achieved_basis": "executed window tests per launch (W per dense (block, sequence) "
+                             "scan + W per sparse-mode candidate check: pms_stats."
+                             "issued_compares) / mean search-kernel event time",
+           "block_scans": int(st.block_scans), "sparse_steps": int(st.sparse_steps),
+           "candidate_checks": int(tests // W - st.block_scans)}
     try:
         r_scan = plan.roofline(1, 64)
         r_pass1 = plan.roofline(0, 256)
+        r_sparse = plan.roofline(2, 64) if st.sparse_steps else None
     except pms.PmsError as e:  # only the slice family has the microbenchmark
         obj.update(peak=None, frac=None, traffic=None, peak_basis=f"n/a ({e})")
         return obj
-    obj.update(peak=r_scan["tests_per_s"] / 1e9, frac=achieved / r_scan["tests_per_s"],
-               peak_basis="measured: pms_plan_roofline mode 1 (R_scan) -- this kernel's "
-                          "per-scan code (prefix test + hit resolution + end of scan) on this "
-                          "instance's tables and hit mix, no work counter / skip rule / "
-                          "hand-off, all SMs, same run",
+    t_ideal = st.block_scans / r_scan["scans_per_s"] + \
+        (st.sparse_steps / r_sparse["scans_per_s"] if r_sparse else 0.0)
+    obj.update(peak=tests / t_ideal / 1e9, frac=t_ideal / t,
+               peak_basis="measured mix roofline: this launch's dense scans at R_scan + its "
+                          "sparse-mode steps at R_sparse (pms_plan_roofline modes 1 and 2: the "
+                          "kernel's own per-unit code on this instance's tables and hit mix, no "
+                          "work counter / skip rule / list extraction, all SMs, same run); "
+                          "peak = executed tests / (scans / R_scan + steps / R_sparse)",
+               ideal_us=t_ideal * 1e6, kernel_us=t * 1e6,
+               r_scan=r_scan["tests_per_s"] / 1e9,
+               r_scan_scans_per_s=r_scan["scans_per_s"],
+               r_sparse_steps_per_s=r_sparse["scans_per_s"] if r_sparse else None,
+               r_sparse=r_sparse["tests_per_s"] / 1e9 if r_sparse else None,
+               dense_share=st.block_scans / r_scan["scans_per_s"] / t,
                r_pass1=r_pass1["tests_per_s"] / 1e9,
-               frac_vs_pass1=achieved / r_pass1["tests_per_s"],
+               frac_vs_pass1=st.block_scans * W / t / r_pass1["tests_per_s"],
                r_pass1_basis="measured: pms_plan_roofline mode 0 -- the bit-sliced prefix "
-                             "test alone (one-hot plane loads + carry-save classification)")
+                             "test alone (one-hot plane loads + carry-save classification); "
+                             "frac_vs_pass1 = dense-scan window tests / time / R_pass1")
     ctx = ncu_context()
     cfg = (ctx or {}).get("config") or {}
     same = (cfg.get("n"), cfg.get("t"), cfg.get("l"), cfg.get("d"), cfg.get("block_digits")) == \
@@ -534,7 +552,9 @@ def run_all_configs(args) -> int:
                    "candidates_per_s": 4 ** l / (med * 1e-3),
                    "executed_tests_per_s": float(np.mean(issued)) / (med * 1e-3),
                    "block_scans": st.block_scans,
-                   "roofline_frac": roof.get("frac"), "r_scan_gtests": roof.get("peak"),
+                   "roofline_frac": roof.get("frac"), "mix_peak_gtests": roof.get("peak"),
+                   "r_scan_gtests": roof.get("r_scan"), "r_sparse_gtests": roof.get("r_sparse"),
+                   "sparse_steps": st.sparse_steps, "dense_share": roof.get("dense_share"),
                    "frac_vs_pass1": roof.get("frac_vs_pass1"),
                    "issue_frac": roof.get("issue", {}).get("frac"),
                    "sm_mhz": cs["sm_mhz"], "clock_samples": cs["samples"],

@@ -151,6 +151,10 @@ typedef struct pms_stats {
                                   parallel (pms_launch.seq_parallel);
                                   bit 1: its hand-off checks ran on the
                                   staged tables (few blocks per warp)       */
+    uint64_t sparse_steps;     /* PMS_ALGO_SLICE sparse mode: (candidate
+                                  list, sequence) steps; each checks the
+                                  list's candidates against W windows (the
+                                  checks are in issued_compares)           */
 } pms_stats;
 
 /* ---------------------------------------------------------------------
@@ -273,8 +277,12 @@ int pms_roofline(int32_t iters, double *compares_per_s,
  *   mode 0: pass 1 only (plane loads + carry-save hit classification): R_pass1
  *   mode 1: pass 1 + hit resolution + end of scan at the instance's own hit
  *           mix: R_scan
- *   tests_per_s  receives (block, sequence) scans * W / second (required)
- *   scans_per_s, ms  scans / second and the kernel time (may be NULL)
+ *   mode 2: sparse-mode steps with lists of the last
+ *           execution's mean list size: R_sparse
+ *   tests_per_s  receives (block, sequence) scans * W / second (required);
+ *                mode 2: candidate-sequence checks * W / second
+ *   scans_per_s, ms  scans (mode 2: sparse steps) / second and the kernel
+ *                time (may be NULL)
  * The tables are placed as the plan's search kernel places them (shared
  * memory, or L1/L2 when they do not fit).  PMS_E_ARG unless the plan runs
  * PMS_ALGO_SLICE and has been executed; CUDA-event timed, best of three

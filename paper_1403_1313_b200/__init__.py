@@ -53,7 +53,7 @@ class Stats(ctypes.Structure):
                 ("generic", ctypes.c_int32), ("table_in_smem", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_uint32), ("algo", ctypes.c_int32),
                 ("block_scans", ctypes.c_uint64), ("block_digits", ctypes.c_int32),
-                ("mode_flags", ctypes.c_int32)]
+                ("mode_flags", ctypes.c_int32), ("sparse_steps", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -264,9 +264,10 @@ class Plan:
                      count.data_ptr(), stream.cuda_stream, wide=wide)
 
     def roofline(self, mode: int, scans_per_warp: int = 64) -> dict:
-        """pms_plan_roofline: the plan's per-scan code without its dynamic
-        parts (mode 0: pass 1 only, R_pass1; mode 1: the whole scan, R_scan)
-        on the tables of its last execution."""
+        """pms_plan_roofline: the plan's per-unit code without its dynamic
+        parts (mode 0: pass 1 only, R_pass1; mode 1: the whole scan, R_scan;
+        mode 2: sparse-mode steps, R_sparse) on the tables of its last
+        execution."""
         a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         s = self._lib.pms_plan_roofline(self._h, int(mode), int(scans_per_warp), ctypes.byref(a),
                                         ctypes.byref(b), ctypes.byref(c))

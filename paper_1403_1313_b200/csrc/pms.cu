@@ -857,6 +857,7 @@ void fill_stats(pms_plan* p, pms_stats* stats) {
                               (p->h_state->extra + p->h_state->block_scans) * W;
     stats->algo = p->algo;
     stats->block_scans = p->h_state->block_scans;
+    stats->sparse_steps = p->h_state->sparse_steps;
     stats->block_digits = p->S;
     stats->mode_flags = (p->seqpar ? 1 : 0) | (p->last_ht ? 2 : 0);
     stats->motifs = 0;
@@ -1256,7 +1257,7 @@ extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compa
 extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_warp,
                                  double* tests_per_s, double* scans_per_s, double* ms) {
     if (!p || !tests_per_s || p->algo != PMS_ALGO_SLICE || !p->executed || mode < 0 ||
-        mode > 1 || scans_per_warp < 1)
+        mode > 2 || scans_per_warp < 1)
         return PMS_E_ARG;
     const SliceRoofFn fn = slice_roofline_kernel(p->S, p->LP, mode, p->in_smem != 0);
     if (!fn) return PMS_E_ARG;
@@ -1278,6 +1279,11 @@ extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_wa
                              smem_optin - (int)fa.sharedSizeBytes) != cudaSuccess)
         return fail_cuda(__LINE__);
     SliceArgs sa = slice_args(p);
+    // mode 2: lists of the last execution's mean sparse list size
+    const int list = hs.sparse_steps
+                         ? std::max(1, std::min(32, (int)std::llround((double)hs.extra / hs.sparse_steps)))
+                         : std::max(1, std::min(32, p->sparse_handoff));
+    if (mode == 2) sa.handoff = list;
     unsigned long long* sink = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (cudaMalloc(&sink, sizeof(unsigned long long)) != cudaSuccess ||
@@ -1303,8 +1309,10 @@ extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_wa
     cudaEventDestroy(e1);
     cudaFree(sink);
     if (err != cudaSuccess) return fail_cuda(__LINE__, err);
+    // modes 0, 1: (block, sequence) scans of W window tests; mode 2: sparse
+    // steps of `list` candidate-sequence checks (W window tests each)
     const double scans = (double)p->grid * (p->block / 32) * scans_per_warp;
-    *tests_per_s = scans * p->W / (best * 1e-3);
+    *tests_per_s = scans * (mode == 2 ? list : 1) * p->W / (best * 1e-3);
     if (scans_per_s) *scans_per_s = scans / (best * 1e-3);
     if (ms) *ms = best;
     return PMS_OK;

@@ -40,7 +40,8 @@ struct DevState {
     unsigned long long extra;   // sequences scanned beyond sequence 0 (survivors)
     unsigned long long block_scans;  // PMS_ALGO_BLOCK (block, sequence) scans
     unsigned int bad;           // = the step's epoch: its pre-pass saw a byte outside ACGTacgt
-    unsigned int pad[3];
+    unsigned int sparse_steps;  // PMS_ALGO_SLICE sparse mode: (list, sequence) steps
+    unsigned int pad[2];
 };
 
 __host__ __device__ __forceinline__ uint32_t compress_even(uint32_t x) {

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kSlicePackThreads) pms_pack_slice(
         st->next = 0ull;
         st->extra = 0ull;
         st->block_scans = 0ull;
+        st->sparse_steps = 0u;
     }
     if (i >= n) return;
     const int Wp = 32 * NWl;
@@ -802,13 +803,70 @@ __device__ __forceinline__ void slice_count3(const uint32_t (&m)[N], uint32_t& s
     s2 = N2 > 0 ? y1[0] : 0u;
 }
 
+// One sparse-mode step: does each of the A listed candidates (suffix codes
+// in the list at L_s) have a window within d in sequence i?  Bit j of the
+// result: candidate j does.
+template <int S, int LP, bool SMEM>
+__device__ __forceinline__ uint32_t slice_sparse_step(const SliceWarp<S, SMEM>& w, const SliceArgs& a,
+                                                      const uint32_t (&po)[LP], int i, uint32_t L_s,
+                                                      uint32_t A) {
+    constexpr uint32_t kGe = 16u + (uint32_t)S;  // K + matches >= 16 + S <=> <= d mismatches
+    const uint32_t lane = w.lane;
+    uint32_t m[LP], c[5];
+    if constexpr (SMEM) {
+        const uint32_t P = w.planes_s + (uint32_t)i * (uint32_t)(LP * 512);
+#pragma unroll
+        for (int j = 0; j < LP; ++j) m[j] = lds32(P + po[j]);
+    } else {
+        const char* P = reinterpret_cast<const char*>(w.planes) + (size_t)i * (LP * 512);
+#pragma unroll
+        for (int j = 0; j < LP; ++j) m[j] = __ldg(reinterpret_cast<const uint32_t*>(P + po[j]));
+    }
+    slice_count<LP>(m, w.km, c);
+    const uint32_t* sp = a.splanes + (size_t)i * (S * 128) + lane;
+    // does the candidate with suffix code x have a window within d here?
+    // (t = c + suffix matches, five planes, no overflow: K + l <= 31;
+    // t >= 16 + S bit-sliced from the low bit up)
+    auto test = [&](const uint32_t (&sm)[S]) -> uint32_t {
+        uint32_t s0, s1, s2;
+        slice_count3<S>(sm, s0, s1, s2);
+        const uint32_t t0 = c[0] ^ s0;
+        uint32_t k = c[0] & s0;
+        const uint32_t t1 = c[1] ^ s1 ^ k;
+        k = (c[1] & s1) | (k & (c[1] ^ s1));
+        const uint32_t t2 = c[2] ^ s2 ^ k;
+        k = (c[2] & s2) | (k & (c[2] ^ s2));
+        const uint32_t t3 = c[3] ^ k;
+        k = c[3] & k;
+        const uint32_t t4 = c[4] | k;
+        const uint32_t t[5] = {t0, t1, t2, t3, t4};
+        uint32_t g = kFull;
+#pragma unroll
+        for (int b = 0; b < 5; ++b) g = ((kGe >> b) & 1u) ? (t[b] & g) : (t[b] | g);
+        return g & w.vmask;
+    };
+    uint32_t keep = 0;
+    // (two candidates per step, their loads overlapped, measured slower:
+    // (15,4) +4 %, (16,5) +1 %)
+#pragma unroll 1
+    for (uint32_t j = 0; j < A; ++j) {
+        const uint32_t x = lds32(L_s + 4u * j);  // broadcast
+        uint32_t sm[S];
+#pragma unroll
+        for (int q = 0; q < S; ++q)
+            sm[q] = __ldg(sp + (q * 4 + ((x >> (2 * (S - 1 - q))) & 3u)) * 32u);
+        keep |= (uint32_t)__any_sync(kFull, test(sm) != 0u) << j;
+    }
+    return keep;
+}
+
 template <int S, int LP, bool SMEM>
 __device__ __forceinline__ void slice_sparse(const SliceWarp<S, SMEM>& w, const SliceArgs& a,
                                              const uint32_t (&po)[LP], int i0,
                                              const uint32_t (&alive)[SliceCfg<S>::KW],
-                                             unsigned long long cbase, unsigned long long& scanned) {
+                                             unsigned long long cbase, unsigned long long& scanned,
+                                             unsigned int& steps) {
     constexpr int KW = SliceCfg<S>::KW;
-    constexpr uint32_t kGe = 16u + (uint32_t)S;  // K + matches >= 16 + S <=> <= d mismatches
     const uint32_t lane = w.lane;
     const uint32_t L_s = w.acc_s;  // the list (the word block is zero here)
     uint32_t A = 0;                 // warp-uniform
@@ -832,51 +890,8 @@ __device__ __forceinline__ void slice_sparse(const SliceWarp<S, SMEM>& w, const 
     const uint32_t A0 = A;
     int i = i0;
     for (; i < a.n && A; ++i) {
-        uint32_t m[LP], c[5];
-        if constexpr (SMEM) {
-            const uint32_t P = w.planes_s + (uint32_t)i * (uint32_t)(LP * 512);
-#pragma unroll
-            for (int j = 0; j < LP; ++j) m[j] = lds32(P + po[j]);
-        } else {
-            const char* P = reinterpret_cast<const char*>(w.planes) + (size_t)i * (LP * 512);
-#pragma unroll
-            for (int j = 0; j < LP; ++j) m[j] = __ldg(reinterpret_cast<const uint32_t*>(P + po[j]));
-        }
-        slice_count<LP>(m, w.km, c);
-        const uint32_t* sp = a.splanes + (size_t)i * (S * 128) + lane;
-        // does the candidate with suffix code x have a window within d here?
-        // (t = c + suffix matches, five planes, no overflow: K + l <= 31;
-        // t >= 16 + S bit-sliced from the low bit up)
-        auto test = [&](const uint32_t (&sm)[S]) -> uint32_t {
-            uint32_t s0, s1, s2;
-            slice_count3<S>(sm, s0, s1, s2);
-            const uint32_t t0 = c[0] ^ s0;
-            uint32_t k = c[0] & s0;
-            const uint32_t t1 = c[1] ^ s1 ^ k;
-            k = (c[1] & s1) | (k & (c[1] ^ s1));
-            const uint32_t t2 = c[2] ^ s2 ^ k;
-            k = (c[2] & s2) | (k & (c[2] ^ s2));
-            const uint32_t t3 = c[3] ^ k;
-            k = c[3] & k;
-            const uint32_t t4 = c[4] | k;
-            const uint32_t t[5] = {t0, t1, t2, t3, t4};
-            uint32_t g = kFull;
-#pragma unroll
-            for (int b = 0; b < 5; ++b) g = ((kGe >> b) & 1u) ? (t[b] & g) : (t[b] | g);
-            return g & w.vmask;
-        };
-        uint32_t keep = 0;
-        // (two candidates per step, their loads overlapped, measured slower:
-        // (15,4) +4 %, (16,5) +1 %)
-#pragma unroll 1
-        for (uint32_t j = 0; j < A; ++j) {
-            const uint32_t x = lds32(L_s + 4u * j);  // broadcast
-            uint32_t sm[S];
-#pragma unroll
-            for (int q = 0; q < S; ++q)
-                sm[q] = __ldg(sp + (q * 4 + ((x >> (2 * (S - 1 - q))) & 3u)) * 32u);
-            keep |= (uint32_t)__any_sync(kFull, test(sm) != 0u) << j;
-        }
+        const uint32_t keep = slice_sparse_step<S, LP, SMEM>(w, a, po, i, L_s, A);
+        ++steps;
         scanned += A;
         // drop the candidates with no window within d in sequence i
         const uint32_t x = lane < A ? lds32(L_s + 4u * lane) : 0u;
@@ -925,6 +940,7 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
     const SliceWarp<S, SMEM> w = slice_setup<S, SMEM>(a, sdyn, &bar, qcnts);
     const uint32_t lane = w.lane;
     unsigned long long scanned = 0, bscans = 0;
+    unsigned int ssteps = 0;  // sparse-mode steps
 #ifdef PMS_TRACE
     const unsigned long long tr_ready = gtimer();
 #endif
@@ -1004,7 +1020,7 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
             if constexpr (!HT) {
                 // throughput instances: sparse mode (the list of at most
                 // a.handoff candidates, all remaining sequences)
-                slice_sparse<S, LP, SMEM>(w, a, po, i, alive, cbase, scanned);
+                slice_sparse<S, LP, SMEM>(w, a, po, i, alive, cbase, scanned, ssteps);
                 continue;
             } else {
                 // latency instances: at most a.handoff survivors, each finished
@@ -1041,6 +1057,7 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
     if (lane == 0) {
         if (scanned) atomicAdd(&a.st->extra, scanned);
         if (bscans) atomicAdd(&a.st->block_scans, bscans);
+        if (ssteps) atomicAdd(&a.st->sparse_steps, ssteps);
     }
 #ifdef PMS_TRACE
     const unsigned long long wg = (unsigned long long)blockIdx.x * NWARP + (threadIdx.x >> 5);
@@ -1153,6 +1170,8 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice_sp(SliceA
 //   MODE 0: pass 1 only (plane loads + carry-save classification) -> R_pass1
 //   MODE 1: pass 1 + hit resolution + end of scan at the instance's own hit
 //           mix (alive reset each scan) -> R_scan
+//   MODE 2: sparse-mode steps, a list of a.handoff candidates per step (the
+//           last execution's mean list size) -> R_sparse
 template <int S, int LP, bool SMEM, int MODE>
 __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceArgs a, int scans,
                                                                         int depth,
@@ -1169,10 +1188,23 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
     uint32_t acc = 0;
     unsigned long long blk = (g * ((nblocks + warps - 1) / warps)) % nblocks;
     int i = 0;
+    const uint32_t A = (uint32_t)min(max(a.handoff, 1), 32);
+    if (MODE == 2 && w.lane < A)  // a fixed pseudo-random candidate list per warp
+        sts32(w.acc_s + 4u * w.lane, (uint32_t)((g * 32u + w.lane) * 2654435761ull) &
+                                         ((1u << (2 * S)) - 1u));
+    __syncwarp();
 #pragma unroll 1
     for (int k = 0; k < scans; ++k) {
         uint32_t po[LP];
         slice_offsets<S, LP>(blk << (2 * S), w.lane, po);
+        if constexpr (MODE == 2) {
+            acc ^= slice_sparse_step<S, LP, SMEM>(w, a, po, i, w.acc_s, A);
+            if (++i == depth) {
+                i = 0;
+                if (++blk == nblocks) blk = 0;
+            }
+            continue;
+        }
         uint32_t c[5], r0m, r1m, r2m, common = 0u;
         slice_pass1<S, LP, SMEM>(w, po, i, c, r0m, r1m, r2m);
         if (MODE == 0) {

@@ -323,3 +323,40 @@ print("ok")
                        env={**os.environ, "PMS_HANDOFF_TABLES": "0"},
                        capture_output=True, text=True, timeout=600)
     assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stderr[-2000:]
+
+
+def test_plan_roofline_modes():
+    """pms_plan_roofline: R_pass1 (mode 0), R_scan (mode 1) and
+    R_sparse (mode 2) on the (15,4) headline instance after an execution;
+    the prefix test alone is faster per window than the whole scan; the
+    plan's next execution is unaffected; bad modes / unexecuted plans are
+    PMS_E_ARG.  The sparse-mode counters are consistent: every step checks
+    at least one candidate."""
+    import torch
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "bj3_seed1.json")))
+    s_np, _ = fmgen.generate_fm(g["n"], g["t"], g["l"], g["d"], g["seed"])
+    dev = torch.device("cuda", 0)
+    s = torch.from_numpy(s_np).to(dev)
+    out = torch.zeros(1 << 16, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    with pms.Plan(g["n"], g["t"], g["l"], g["d"]) as plan:
+        with pytest.raises(pms.PmsError):
+            plan.roofline(1, 4)  # not executed yet
+        plan.execute_tensors(s, out, cnt)
+        status, st = plan.wait()
+        assert status == 0 and st.algo == pms.ALGO_SLICE
+        W = g["t"] - g["l"] + 1
+        checks = st.issued_compares // W - st.block_scans
+        assert st.sparse_steps > 0 and checks >= st.sparse_steps
+        r0, r1, r2 = plan.roofline(0, 16), plan.roofline(1, 16), plan.roofline(2, 16)
+        for r in (r0, r1, r2):
+            assert r["tests_per_s"] > 0 and r["scans_per_s"] > 0 and r["ms"] > 0
+        assert r0["tests_per_s"] > r1["tests_per_s"]
+        for bad in (-1, 3):
+            with pytest.raises(pms.PmsError):
+                plan.roofline(bad, 4)
+        plan.execute_tensors(s, out, cnt)
+        status, st2 = plan.wait()
+        assert status == 0
+        assert sorted(out[:int(cnt.item())].cpu().numpy().astype(np.uint32).tolist()) == g["codes"]
+        assert (st2.block_scans, st2.sparse_steps) == (st.block_scans, st.sparse_steps)
