@@ -658,6 +658,12 @@ extern "C" void pms_plan_destroy(pms_plan* plan) { destroy_plan(plan); }
 
 namespace {
 
+// DevState.extra: per-candidate sequence checks (low bits) | the slice
+// family's sparse-mode steps << kSparseStepShift
+unsigned long long extra_checks(const DevState& s) {
+    return s.extra & ((1ull << kSparseStepShift) - 1ull);
+}
+
 // The slice kernels' arguments that depend on the plan only (tables, shape,
 // threshold masks, skip rule and hand-off).
 SliceArgs slice_args(const pms_plan* p) {
@@ -854,10 +860,10 @@ void fill_stats(pms_plan* p, pms_stats* stats) {
     stats->issued_compares =
         p->h_state->bad == p->epoch ? 0
                         : (seq0_implicit ? cands * W : 0) +
-                              (p->h_state->extra + p->h_state->block_scans) * W;
+                              (extra_checks(*p->h_state) + p->h_state->block_scans) * W;
     stats->algo = p->algo;
     stats->block_scans = p->h_state->block_scans;
-    stats->sparse_steps = p->h_state->sparse_steps;
+    stats->sparse_steps = p->h_state->extra >> kSparseStepShift;
     stats->block_digits = p->S;
     stats->mode_flags = (p->seqpar ? 1 : 0) | (p->last_ht ? 2 : 0);
     stats->motifs = 0;
@@ -1280,8 +1286,9 @@ extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_wa
         return fail_cuda(__LINE__);
     SliceArgs sa = slice_args(p);
     // mode 2: lists of the last execution's mean sparse list size
-    const int list = hs.sparse_steps
-                         ? std::max(1, std::min(32, (int)std::llround((double)hs.extra / hs.sparse_steps)))
+    const unsigned long long ssteps = hs.extra >> kSparseStepShift;
+    const int list = ssteps
+                         ? std::max(1, std::min(32, (int)std::llround((double)extra_checks(hs) / ssteps)))
                          : std::max(1, std::min(32, p->sparse_handoff));
     if (mode == 2) sa.handoff = list;
     unsigned long long* sink = nullptr;

@@ -35,13 +35,15 @@ static __device__ unsigned int g_pms_violations;  // one per translation unit
     } while (0)
 #endif
 
+constexpr int kSparseStepShift = 40;  // DevState.extra: candidate checks | steps << 40
 struct DevState {
     unsigned long long next;    // work counter: candidates handed out, from lo_al
-    unsigned long long extra;   // sequences scanned beyond sequence 0 (survivors)
+    unsigned long long extra;   // sequences scanned beyond sequence 0 (survivors); the slice
+                                // family's sparse-mode steps count from bit kSparseStepShift
+
     unsigned long long block_scans;  // PMS_ALGO_BLOCK (block, sequence) scans
     unsigned int bad;           // = the step's epoch: its pre-pass saw a byte outside ACGTacgt
-    unsigned int sparse_steps;  // PMS_ALGO_SLICE sparse mode: (list, sequence) steps
-    unsigned int pad[2];
+    unsigned int pad[3];
 };
 
 __host__ __device__ __forceinline__ uint32_t compress_even(uint32_t x) {

@@ -181,7 +181,6 @@ __global__ void __launch_bounds__(kPackThreads) pms_pack_kernel(
         st->next = 0ull;
         st->extra = 0ull;
         st->block_scans = 0ull;
-        st->sparse_steps = 0u;
     }
     if (i >= n) return;
     // bytes [s0, s1) of row i feed windows k0 .. k0 + kPackThreads - 1 (clamped to W-1)

@@ -201,7 +201,6 @@ __global__ void __launch_bounds__(kSlicePackThreads) pms_pack_slice(
         st->next = 0ull;
         st->extra = 0ull;
         st->block_scans = 0ull;
-        st->sparse_steps = 0u;
     }
     if (i >= n) return;
     const int Wp = 32 * NWl;
@@ -864,8 +863,7 @@ template <int S, int LP, bool SMEM>
 __device__ __forceinline__ void slice_sparse(const SliceWarp<S, SMEM>& w, const SliceArgs& a,
                                              const uint32_t (&po)[LP], int i0,
                                              const uint32_t (&alive)[SliceCfg<S>::KW],
-                                             unsigned long long cbase, unsigned long long& scanned,
-                                             unsigned int& steps) {
+                                             unsigned long long cbase, unsigned long long& scanned) {
     constexpr int KW = SliceCfg<S>::KW;
     const uint32_t lane = w.lane;
     const uint32_t L_s = w.acc_s;  // the list (the word block is zero here)
@@ -891,8 +889,9 @@ __device__ __forceinline__ void slice_sparse(const SliceWarp<S, SMEM>& w, const 
     int i = i0;
     for (; i < a.n && A; ++i) {
         const uint32_t keep = slice_sparse_step<S, LP, SMEM>(w, a, po, i, L_s, A);
-        ++steps;
-        scanned += A;
+        // candidate checks in the low bits, steps from bit kSparseStepShift
+        // (DevState.extra; the host splits them)
+        scanned += A + (1ull << kSparseStepShift);
         // drop the candidates with no window within d in sequence i
         const uint32_t x = lane < A ? lds32(L_s + 4u * lane) : 0u;
         __syncwarp();
@@ -940,7 +939,6 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
     const SliceWarp<S, SMEM> w = slice_setup<S, SMEM>(a, sdyn, &bar, qcnts);
     const uint32_t lane = w.lane;
     unsigned long long scanned = 0, bscans = 0;
-    unsigned int ssteps = 0;  // sparse-mode steps
 #ifdef PMS_TRACE
     const unsigned long long tr_ready = gtimer();
 #endif
@@ -1020,7 +1018,7 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
             if constexpr (!HT) {
                 // throughput instances: sparse mode (the list of at most
                 // a.handoff candidates, all remaining sequences)
-                slice_sparse<S, LP, SMEM>(w, a, po, i, alive, cbase, scanned, ssteps);
+                slice_sparse<S, LP, SMEM>(w, a, po, i, alive, cbase, scanned);
                 continue;
             } else {
                 // latency instances: at most a.handoff survivors, each finished
@@ -1057,7 +1055,6 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
     if (lane == 0) {
         if (scanned) atomicAdd(&a.st->extra, scanned);
         if (bscans) atomicAdd(&a.st->block_scans, bscans);
-        if (ssteps) atomicAdd(&a.st->sparse_steps, ssteps);
     }
 #ifdef PMS_TRACE
     const unsigned long long wg = (unsigned long long)blockIdx.x * NWARP + (threadIdx.x >> 5);
