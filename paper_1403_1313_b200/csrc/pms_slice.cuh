@@ -111,6 +111,9 @@ constexpr int kSliceMaxLP = 11;              // l <= 16, S >= 5
 #ifndef PMS_SLICE_R0_DIRECT
 #define PMS_SLICE_R0_DIRECT 1  // r = 0 hits resolved per lane (no queue); 0: queued
 #endif
+#ifndef PMS_SLICE_R0_PAIR
+#define PMS_SLICE_R0_PAIR 1  // r = 0 loop: two hits per iteration (duplicate reds are idempotent)
+#endif
 #ifndef PMS_SLICE_EXCH
 #define PMS_SLICE_EXCH 1  // end of scan: atom.exch(word, 0) instead of load + store
 #endif
@@ -550,12 +553,26 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
     // and a share of a round (~16); the kernel is issue-bound, not LSU-bound
     {
         const uint32_t acc = w.acc_s;
+#if PMS_SLICE_R0_PAIR
+        // two hits per iteration: both slot loads in flight together (the
+        // second is a repeat of the first when the lane has one hit left)
+        while (r0m) {
+            const int q = msb(r0m);
+            r0m ^= 1u << q;
+            const int q2 = r0m ? msb(r0m) : q;
+            r0m &= ~(1u << q2);
+            const uint32_t sl = slot_of(q), sl2 = slot_of(q2);
+            red_or(acc | (sl & 0x7FFu), 1u << (sl >> 11));
+            red_or(acc | (sl2 & 0x7FFu), 1u << (sl2 >> 11));
+        }
+#else
         while (r0m) {
             const int q = msb(r0m);
             r0m ^= 1u << q;
             const uint32_t sl = slot_of(q);
             red_or(acc | (sl & 0x7FFu), 1u << (sl >> 11));
         }
+#endif
 #if PMS_SLICE_R1_DIRECT
         while (r1m) {
             const int q = msb(r1m);
