@@ -214,17 +214,18 @@ def roofline_object(pms, plan, st, search_ms: float, clk: dict, sms: int) -> dic
     test, done two ways): dense (block, sequence) scans -- W window tests
     against a block's shared prefix, hits resolved as Hamming balls -- and
     sparse-mode steps -- a short list of candidates each tested against W
-    windows.  Each kind has a measured microbenchmark of the kernel's own code
-    for that unit on this instance's tables, all SMs, same run:
-    R_scan (pms_plan_roofline mode 1) and R_sparse (mode 2).  The ideal time
-    is scans / R_scan + steps / R_sparse; frac = ideal / measured kernel time
-    (what the dynamic parts -- work counter, skip rule, list extraction,
-    load balance, tail -- cost).  achieved = executed window tests (W per scan
-    and per candidate check, pms_stats.issued_compares) / kernel time; peak =
-    the same tests / the ideal time.  Also reported: R_pass1 (mode 0, the
-    prefix test alone) with frac_vs_pass1 = dense-scan tests / R_pass1, and
-    the hardware issue roofline (ncu warp instructions of this launch / 4
-    warp-instructions/clk/SM x SMs x the sampled clock)."""
+    windows.  achieved = executed window tests (W per scan and per candidate
+    check, pms_stats.issued_compares) / mean kernel event time.
+    peak = R_mix (pms_plan_roofline mode 3): a microbenchmark of the kernel's
+    own code for both units, interleaved at this launch's own ratio (sparse
+    steps per scan, mean list size), on this instance's tables and hit mix,
+    with the dynamic parts removed (work counter, skip rule, list
+    extraction, output), every warp busy, all SMs, same run -- the north
+    star's "microbenchmark of the same instruction mix".  frac = achieved /
+    R_mix.  Also reported: R_scan and R_sparse (modes 1, 2: each unit alone),
+    R_pass1 (mode 0, the prefix test alone) with frac_vs_pass1 = dense-scan
+    tests / R_pass1, and the hardware issue roofline (ncu warp instructions of
+    this launch / 4 warp-instructions/clk/SM x SMs x the sampled clock)."""
     W = plan.t - plan.l + 1
     t = search_ms * 1e-3
     tests = st.issued_compares
@@ -235,25 +236,27 @@ def roofline_object(pms, plan, st, search_ms: float, clk: dict, sms: int) -> dic
            "block_scans": int(st.block_scans), "sparse_steps": int(st.sparse_steps),
            "candidate_checks": int(tests // W - st.block_scans)}
     try:
+        r_mix = plan.roofline(3, 64)
         r_scan = plan.roofline(1, 64)
         r_pass1 = plan.roofline(0, 256)
         r_sparse = plan.roofline(2, 64) if st.sparse_steps else None
     except pms.PmsError as e:  # only the slice family has the microbenchmark
         obj.update(peak=None, frac=None, traffic=None, peak_basis=f"n/a ({e})")
         return obj
-    t_ideal = st.block_scans / r_scan["scans_per_s"] + \
+    t_sep = st.block_scans / r_scan["scans_per_s"] + \
         (st.sparse_steps / r_sparse["scans_per_s"] if r_sparse else 0.0)
-    obj.update(peak=tests / t_ideal / 1e9, frac=t_ideal / t,
-               peak_basis="measured mix roofline: this launch's dense scans at R_scan + its "
-                          "sparse-mode steps at R_sparse (pms_plan_roofline modes 1 and 2: the "
-                          "kernel's own per-unit code on this instance's tables and hit mix, no "
-                          "work counter / skip rule / list extraction, all SMs, same run); "
-                          "peak = executed tests / (scans / R_scan + steps / R_sparse)",
-               ideal_us=t_ideal * 1e6, kernel_us=t * 1e6,
+    obj.update(peak=r_mix["tests_per_s"] / 1e9, frac=tests / t / r_mix["tests_per_s"],
+               peak_basis="measured: pms_plan_roofline mode 3 (R_mix) -- this kernel's dense "
+                          "scans with its sparse-mode steps interleaved at this launch's ratio "
+                          "and list size, its own code on this instance's tables and hit mix, "
+                          "no work counter / skip rule / list extraction / output, all SMs, "
+                          "same run",
                r_scan=r_scan["tests_per_s"] / 1e9,
-               r_scan_scans_per_s=r_scan["scans_per_s"],
-               r_sparse_steps_per_s=r_sparse["scans_per_s"] if r_sparse else None,
                r_sparse=r_sparse["tests_per_s"] / 1e9 if r_sparse else None,
+               separate_units_us=t_sep * 1e6, kernel_us=t * 1e6,
+               separate_units_note="scans / R_scan + steps / R_sparse: each unit measured "
+                                   "alone; latency-bound sparse steps overlap dense scans of "
+                                   "other warps in the kernel, so this can exceed R_mix's time",
                dense_share=st.block_scans / r_scan["scans_per_s"] / t,
                r_pass1=r_pass1["tests_per_s"] / 1e9,
                frac_vs_pass1=st.block_scans * W / t / r_pass1["tests_per_s"],
@@ -552,7 +555,7 @@ def run_all_configs(args) -> int:
                    "candidates_per_s": 4 ** l / (med * 1e-3),
                    "executed_tests_per_s": float(np.mean(issued)) / (med * 1e-3),
                    "block_scans": st.block_scans,
-                   "roofline_frac": roof.get("frac"), "mix_peak_gtests": roof.get("peak"),
+                   "roofline_frac": roof.get("frac"), "r_mix_gtests": roof.get("peak"),
                    "r_scan_gtests": roof.get("r_scan"), "r_sparse_gtests": roof.get("r_sparse"),
                    "sparse_steps": st.sparse_steps, "dense_share": roof.get("dense_share"),
                    "frac_vs_pass1": roof.get("frac_vs_pass1"),

@@ -279,8 +279,11 @@ int pms_roofline(int32_t iters, double *compares_per_s,
  *           mix: R_scan
  *   mode 2: sparse-mode steps with lists of the last
  *           execution's mean list size: R_sparse
+ *   mode 3: dense scans with the last execution's sparse steps per scan
+ *           interleaved (its own mix of both units): R_mix
  *   tests_per_s  receives (block, sequence) scans * W / second (required);
- *                mode 2: candidate-sequence checks * W / second
+ *                mode 2: candidate-sequence checks * W / second; mode 3:
+ *                (scans + checks) * W / second
  *   scans_per_s, ms  scans (mode 2: sparse steps) / second and the kernel
  *                time (may be NULL)
  * The tables are placed as the plan's search kernel places them (shared

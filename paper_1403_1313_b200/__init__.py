@@ -266,8 +266,8 @@ class Plan:
     def roofline(self, mode: int, scans_per_warp: int = 64) -> dict:
         """pms_plan_roofline: the plan's per-unit code without its dynamic
         parts (mode 0: pass 1 only, R_pass1; mode 1: the whole scan, R_scan;
-        mode 2: sparse-mode steps, R_sparse) on the tables of its last
-        execution."""
+        mode 2: sparse-mode steps, R_sparse; mode 3: both interleaved at the
+        last execution's ratio, R_mix) on the tables of its last execution."""
         a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         s = self._lib.pms_plan_roofline(self._h, int(mode), int(scans_per_warp), ctypes.byref(a),
                                         ctypes.byref(b), ctypes.byref(c))

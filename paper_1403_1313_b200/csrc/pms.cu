@@ -1263,7 +1263,7 @@ extern "C" int pms_roofline(int32_t iters, double* compares_per_s, double* compa
 extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_warp,
                                  double* tests_per_s, double* scans_per_s, double* ms) {
     if (!p || !tests_per_s || p->algo != PMS_ALGO_SLICE || !p->executed || mode < 0 ||
-        mode > 2 || scans_per_warp < 1)
+        mode > 3 || scans_per_warp < 1)
         return PMS_E_ARG;
     const SliceRoofFn fn = slice_roofline_kernel(p->S, p->LP, mode, p->in_smem != 0);
     if (!fn) return PMS_E_ARG;
@@ -1290,7 +1290,11 @@ extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_wa
     const int list = ssteps
                          ? std::max(1, std::min(32, (int)std::llround((double)extra_checks(hs) / ssteps)))
                          : std::max(1, std::min(32, p->sparse_handoff));
-    if (mode == 2) sa.handoff = list;
+    if (mode >= 2) sa.handoff = list;
+    // mode 3: sparse steps per dense scan of the last execution, 16.16
+    const double ratio = hs.block_scans ? (double)ssteps / (double)hs.block_scans : 0.0;
+    const uint32_t ratio_fp = (uint32_t)std::min(65536.0 * 64, std::llround(ratio * 65536.0) * 1.0);
+    if (mode == 3) sa.batch = (int)ratio_fp;
     unsigned long long* sink = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (cudaMalloc(&sink, sizeof(unsigned long long)) != cudaSuccess ||
@@ -1318,8 +1322,17 @@ extern "C" int pms_plan_roofline(pms_plan* p, int32_t mode, int32_t scans_per_wa
     if (err != cudaSuccess) return fail_cuda(__LINE__, err);
     // modes 0, 1: (block, sequence) scans of W window tests; mode 2: sparse
     // steps of `list` candidate-sequence checks (W window tests each)
-    const double scans = (double)p->grid * (p->block / 32) * scans_per_warp;
-    *tests_per_s = scans * (mode == 2 ? list : 1) * p->W / (best * 1e-3);
+    const double warps = (double)p->grid * (p->block / 32);
+    const double scans = warps * scans_per_warp;
+    // mode 3: the warps' sparse steps, as their credit loops count them
+    // (warp g starts with credit (g * 40503) mod 2^16)
+    double steps3 = 0.0;
+    for (uint64_t g = 0; g < (uint64_t)warps; ++g)
+        steps3 += (double)((((g * 40503u) & 0xFFFFu) + (uint64_t)scans_per_warp * ratio_fp) >> 16);
+    *tests_per_s = (mode == 2   ? scans * list
+                    : mode == 3 ? scans + steps3 * list
+                                : scans) *
+                   p->W / (best * 1e-3);
     if (scans_per_s) *scans_per_s = scans / (best * 1e-3);
     if (ms) *ms = best;
     return PMS_OK;

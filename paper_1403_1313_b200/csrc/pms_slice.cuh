@@ -1175,9 +1175,9 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice_sp(SliceA
 // ------------------------------------------------- roofline microbenchmark
 // The search kernel's per-scan code on the same tables, with everything
 // dynamic removed: no work counter, no skip rule, no hand-off, no output.
-// Warp g walks consecutive blocks from its own region of the code space (as
-// the search's batches do: neighbouring blocks share all but the last prefix
-// digit, hence most plane rows) and scans each against sequences 0 ..
+// Warp g walks blocks g, g + warps, g + 2 warps, ... (as the search's
+// one-block grabs do: the warps running at any time hold neighbouring blocks,
+// which share most plane rows) and scans each against sequences 0 ..
 // depth-1, depth = the last execution's scans per block (the mix the skip
 // rule produced); every warp stays busy for `scans` scans.  Both matter
 // when the tables are read through L1/L2.
@@ -1186,6 +1186,8 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice_sp(SliceA
 //           mix (alive reset each scan) -> R_scan
 //   MODE 2: sparse-mode steps, a list of a.handoff candidates per step (the
 //           last execution's mean list size) -> R_sparse
+//   MODE 3: the launch's own mix: MODE 1 scans with a.batch / 65536 sparse
+//           steps interleaved per scan (the last execution's ratio) -> R_mix
 template <int S, int LP, bool SMEM, int MODE>
 __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceArgs a, int scans,
                                                                         int depth,
@@ -1200,13 +1202,18 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
     const unsigned long long warps = (unsigned long long)gridDim.x * NWARP;
     const unsigned long long g = (unsigned long long)blockIdx.x * NWARP + (threadIdx.x >> 5);
     uint32_t acc = 0;
-    unsigned long long blk = (g * ((nblocks + warps - 1) / warps)) % nblocks;
+    unsigned long long blk = g % nblocks;
     int i = 0;
     const uint32_t A = (uint32_t)min(max(a.handoff, 1), 32);
-    if (MODE == 2 && w.lane < A)  // a fixed pseudo-random candidate list per warp
-        sts32(w.acc_s + 4u * w.lane, (uint32_t)((g * 32u + w.lane) * 2654435761ull) &
-                                         ((1u << (2 * S)) - 1u));
+    // a fixed pseudo-random candidate list per warp (modes 2, 3)
+    const uint32_t xl = (uint32_t)((g * 32u + w.lane) * 2654435761ull) & ((1u << (2 * S)) - 1u);
+    if (MODE == 2 && w.lane < A) sts32(w.acc_s + 4u * w.lane, xl);
     __syncwarp();
+    // mode 3: sparse steps owed, 16.16 fixed point (a.batch per scan); the
+    // warps start at staggered fractions, so their sparse steps do not all
+    // fall on the same scans (in the search they come whenever a block's
+    // survivors drop below the threshold)
+    uint32_t credit = (uint32_t)(g * 40503u) & 0xFFFFu;
 #pragma unroll 1
     for (int k = 0; k < scans; ++k) {
         uint32_t po[LP];
@@ -1215,7 +1222,7 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
             acc ^= slice_sparse_step<S, LP, SMEM>(w, a, po, i, w.acc_s, A);
             if (++i == depth) {
                 i = 0;
-                if (++blk == nblocks) blk = 0;
+                blk = (blk + warps) % nblocks;
             }
             continue;
         }
@@ -1229,10 +1236,27 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
 #pragma unroll
             for (int q = 0; q < KW; ++q) alive[q] = kFull;
             acc += (uint32_t)slice_finish<S, SMEM>(w, common, alive, a.handoff);
+            if constexpr (MODE == 3) {
+                // the launch's own mix: a.batch / 65536 sparse steps per dense
+                // scan, interleaved, the list written into the (zero) word
+                // block and cleared again as the search kernel does
+                credit += (uint32_t)a.batch;
+                if (credit >= 65536u) {
+                    if (w.lane < A) sts32(w.acc_s + 4u * w.lane, xl);
+                    __syncwarp();
+                    do {
+                        credit -= 65536u;
+                        acc ^= slice_sparse_step<S, LP, SMEM>(w, a, po, i, w.acc_s, A);
+                    } while (credit >= 65536u);
+                    __syncwarp();
+                    if (w.lane < A) sts32(w.acc_s + 4u * w.lane, 0u);
+                    __syncwarp();
+                }
+            }
         }
         if (++i == depth) {
             i = 0;
-            if (++blk == nblocks) blk = 0;
+            blk = (blk + warps) % nblocks;
         }
     }
     if (acc == 0x9E3779B9u) sink[0] = acc;  // keeps the work live

@@ -1,7 +1,8 @@
 """Render BASELINE.md's results table from a bench.py --all-configs document
 (profiles/r02_configs.json): every config x seed, search time, rates, the
-roofline fraction (vs the measured mix roofline: dense scans at R_scan +
-sparse-mode steps at R_sparse) and the oracle timings.
+roofline fraction (vs the measured R_mix microbenchmark: the kernel's dense
+scans with its sparse-mode steps interleaved at the run's own ratio) and the
+oracle timings.
     python scripts/baseline_table.py profiles/r02_configs.json"""
 import json
 import sys
@@ -9,7 +10,7 @@ import sys
 d = json.load(open(sys.argv[1]))
 orc = {o["config"]: o for o in d["oracle"]["rows"]}
 cores = d["oracle"]["cores"]
-print("| Config | seed | GPU search ms (median / mean of 9) | candidates/s | skip-BF-equivalent compares/s (C_alg / t) | executed window tests/s | frac of mix roofline | frac of R_pass1 | SM MHz | oracle s (%d cores) | oracle candidates/s | parity |" % cores)
+print("| Config | seed | GPU search ms (median / mean of 9) | candidates/s | skip-BF-equivalent compares/s (C_alg / t) | executed window tests/s | frac of R_mix | frac of R_pass1 | SM MHz | oracle s (%d cores) | oracle candidates/s | parity |" % cores)
 print("|---|---|---|---|---|---|---|---|---|---|---|---|")
 for r in d["rows"]:
     o = orc.get(r["config"]) if r["seed"] == 1 else None

@@ -326,8 +326,9 @@ print("ok")
 
 
 def test_plan_roofline_modes():
-    """pms_plan_roofline: R_pass1 (mode 0), R_scan (mode 1) and
-    R_sparse (mode 2) on the (15,4) headline instance after an execution;
+    """pms_plan_roofline: R_pass1 (mode 0), R_scan (mode 1),
+    R_sparse (mode 2) and R_mix (mode 3) on the (15,4) headline instance after
+    an execution;
     the prefix test alone is faster per window than the whole scan; the
     plan's next execution is unaffected; bad modes / unexecuted plans are
     PMS_E_ARG.  The sparse-mode counters are consistent: every step checks
@@ -348,11 +349,11 @@ def test_plan_roofline_modes():
         W = g["t"] - g["l"] + 1
         checks = st.issued_compares // W - st.block_scans
         assert st.sparse_steps > 0 and checks >= st.sparse_steps
-        r0, r1, r2 = plan.roofline(0, 16), plan.roofline(1, 16), plan.roofline(2, 16)
-        for r in (r0, r1, r2):
+        r0, r1, r2, r3 = (plan.roofline(m, 16) for m in range(4))
+        for r in (r0, r1, r2, r3):
             assert r["tests_per_s"] > 0 and r["scans_per_s"] > 0 and r["ms"] > 0
         assert r0["tests_per_s"] > r1["tests_per_s"]
-        for bad in (-1, 3):
+        for bad in (-1, 4):
             with pytest.raises(pms.PmsError):
                 plan.roofline(bad, 4)
         plan.execute_tensors(s, out, cnt)
