@@ -1100,17 +1100,27 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice_sp(SliceA
     extern __shared__ __align__(128) uint32_t sdyn[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t qcnts[NWARP];
+#ifdef PMS_TRACE
+    const unsigned long long tr_enter = gtimer();
+    unsigned long long tr_units = 0;
+#endif
     pdl_wait();
     if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
     const SliceWarp<S, true> w = slice_setup<S, true>(a, sdyn, &bar, qcnts);
     const uint32_t lane = w.lane;
     const unsigned long long nunits = a.sp_blocks * (unsigned long long)a.n;
     unsigned long long bscans = 0;
+#ifdef PMS_TRACE
+    const unsigned long long tr_ready = gtimer();
+#endif
     for (;;) {
         unsigned long long u = 0;
         if (lane == 0) u = atomicAdd(&a.st->next, 1ull);
         u = __shfl_sync(kFull, u, 0);
         if (u >= nunits) break;
+#ifdef PMS_TRACE
+        ++tr_units;
+#endif
         const unsigned long long b = u / (unsigned)a.n;
         const int i = (int)(u - b * (unsigned)a.n);
         const unsigned long long cbase = a.lo_al + (b << (2 * S));
@@ -1170,6 +1180,14 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice_sp(SliceA
         }
     }
     if (lane == 0 && bscans) atomicAdd(&a.st->block_scans, bscans);
+#ifdef PMS_TRACE
+    const unsigned long long wg = (unsigned long long)blockIdx.x * NWARP + (threadIdx.x >> 5);
+    if (lane == 0 && wg < 8192) {  // [enter, ready, end, units, scans, 0, 0, 0]
+        unsigned long long* r = g_pms_trace + wg * 8;
+        r[0] = tr_enter; r[1] = tr_ready; r[2] = gtimer(); r[3] = tr_units;
+        r[4] = bscans; r[5] = 0; r[6] = 0; r[7] = 0;
+    }
+#endif
 }
 
 // ------------------------------------------------- roofline microbenchmark

@@ -22,9 +22,10 @@ ap.add_argument("--configs", default="1,2,3")
 ap.add_argument("--variants", default="")
 ap.add_argument("--defs", default="")
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--lib", default="", help="a prebuilt -DPMS_TRACE library (skip the build)")
 args = ap.parse_args()
 
-lib = subprocess.check_output([sys.executable, os.path.join(ROOT, "scripts", "variants.py"), "build",
+lib = args.lib or subprocess.check_output([sys.executable, os.path.join(ROOT, "scripts", "variants.py"), "build",
                                "trace", "-DPMS_TRACE"] + args.defs.split()).decode().split()[-1]
 os.environ["PMS_LIB_OVERRIDE"] = lib
 
