@@ -23,9 +23,10 @@ if _ovr:
         raise RuntimeError(f"PMS_LIB_OVERRIDE must name build/variants/*/libpms_b200.so, got {_ovr!r}")
     LIB = _real
 # pms.cu: 32-bit-word kernels + host code; pms64.cu: 64-bit-word kernels (l <= 31);
-# pms_slice.cu / pms_roof.cu: the slice family's kernels and roofline kernels
+# pms_slice.cu / pms_slice_ht.cu / pms_slice_wide.cu (l = 17..31) / pms_roof.cu: the
+# slice family's kernels and roofline kernels
 SOURCES = [os.path.join(CSRC, f) for f in ("pms.cu", "pms64.cu", "pms_slice.cu",
-                                              "pms_slice_ht.cu", "pms_roof.cu")]
+                                              "pms_slice_ht.cu", "pms_slice_wide.cu", "pms_roof.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, h) for h in ("pms_device.cuh", "pms_kernels.cuh",
                                                     "pms_slice.cuh")] + \
     [os.path.join(ROOT, "include", "pms.h")]

@@ -155,6 +155,9 @@ const SliceKernel* find_slice_kernel(int S, int LP) {
     const SliceKernel* ks = slice_kernels(&cnt);
     for (int q = 0; q < cnt; ++q)
         if (ks[q].S == S && ks[q].LP == LP) return &ks[q];
+    ks = slice_kernels_wide(&cnt);  // l = 17..31
+    for (int q = 0; q < cnt; ++q)
+        if (ks[q].S == S && ks[q].LP == LP) return &ks[q];
     return nullptr;
 }
 
@@ -417,11 +420,15 @@ extern "C" int pms_plan_create(int32_t n, int32_t t, int32_t l, int32_t d,
     const int S_slice = p->launch.block_digits >= 5 && p->launch.block_digits <= 7
                             ? p->launch.block_digits
                             : (l >= 13 ? 7 : S);
-    // PMS_ALGO_SLICE (the default where it applies): 32-bit codes, rows of at
-    // most 1024 windows, a prefix of 1..11 digits with d below its length
-    // (otherwise every window would hit); elsewhere the block family runs
-    if (block_algo && p->launch.algo != PMS_ALGO_BLOCK && !p->wide && p->W <= 1024 &&
-        l - S_slice >= 1 && d < l - S_slice && find_slice_kernel(S_slice, l - S_slice)) {
+    // PMS_ALGO_SLICE (the default where it applies): l <= 31, rows of at most
+    // 1024 windows, a prefix of LP = l - S digits with d below it (otherwise
+    // every window would hit), within the prefix counter's range (LP - d <= 16,
+    // d <= 15: K + LP <= 31) and an instance for (S, LP) (l = 17..31: S = 7,
+    // pms_slice_wide.cu); wide_words asks for the block family's 64-bit words;
+    // elsewhere the block family runs
+    if (block_algo && p->launch.algo != PMS_ALGO_BLOCK && !p->launch.wide_words && p->W <= 1024 &&
+        l - S_slice >= 1 && d < l - S_slice && l - S_slice - d <= 16 && d <= 15 &&
+        find_slice_kernel(S_slice, l - S_slice)) {
         S = S_slice;
         const SliceKernel* sk = find_slice_kernel(S, l - S);
         p->algo = PMS_ALGO_SLICE;
@@ -751,6 +758,9 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
         // kSparseHandoff candidates together
         if (p->launch.handoff <= 0) sa.handoff = ht ? (p->d >= 5 ? 2 : 1) : p->sparse_handoff;
         if (!ht && sa.handoff > 32) sa.handoff = 32;  // one sparse list entry per lane
+        // the sparse test adds the suffix matches to the prefix counter: K + l
+        // = 16 + d + S must stay below 32 (large l and d: dense scans only)
+        if (!ht && p->d + p->S > 15) sa.handoff = 0;
         int sp_words = 0, sp_blocks = 0;
         if (p->seqpar) {
             sa.spmask = p->d_spmask;
@@ -1352,7 +1362,8 @@ extern "C" int64_t pms_debug_violations(int32_t reset) {
     int64_t total = (int64_t)v;
     for (int64_t x : {pms::debug_violations64(reset), pms::debug_violations_slice(reset),
                       pms::debug_violations_roof(reset),
-                      pms::debug_violations_ht(reset)}) {  // the other TUs' counters
+                      pms::debug_violations_ht(reset),
+                      pms::debug_violations_wide(reset)}) {  // the other TUs' counters
         if (x < 0) return x;
         total += x;
     }

@@ -88,6 +88,7 @@ struct SliceKernel {
     SliceFn fn_smem, fn_global;
 };
 const SliceKernel* slice_kernels(int* count);              // pms_slice.cu
+const SliceKernel* slice_kernels_wide(int* count);         // pms_slice_wide.cu (l = 17..31)
 SliceFn slice_seqpar_kernel(int S, int LP);                // pms_slice.cu (staged tables)
 SliceFn slice_ht_kernel(int S, int LP);                    // pms_slice_ht.cu (staged tables,
                                                            // hand-off on the tables)
@@ -96,6 +97,7 @@ SliceRoofFn slice_roofline_kernel(int S, int LP, int mode, bool smem);  // pms_r
 int64_t debug_violations_slice(int reset);
 int64_t debug_violations_roof(int reset);
 int64_t debug_violations_ht(int reset);
+int64_t debug_violations_wide(int reset);
 
 // Slice ball table: T[rho][e][m] (rho = 0..6, as pms_search_block's) then the
 // radius-1 rows R1[e][u] (kSR1Stride words per e): u = 0: T[1][e][0]; u = 1..5:
@@ -107,7 +109,7 @@ constexpr int kSR1Off = 7 * 1024;
 // conflicts on the row loads, ncu source page)
 constexpr int kSR1Stride = 17;
 constexpr int kSTWords = kSR1Off + 32 * kSR1Stride;  // 30.1 KB
-constexpr int kSliceMaxLP = 11;              // l <= 16, S >= 5
+constexpr int kSliceMaxLP = 24;              // l <= 31 (S = 7); LP - d <= 16, d <= 15
 #ifndef PMS_SLICE_R0_DIRECT
 #define PMS_SLICE_R0_DIRECT 1  // r = 0 hits resolved per lane (no queue); 0: queued
 #endif
@@ -270,7 +272,8 @@ __device__ __forceinline__ uint32_t csa_col(uint32_t* v, uint32_t* cy) {
 }
 
 // K + (number of set planes among m[0..LP)) as five bit planes c[0..4],
-// K given by its four bit masks (K <= 15, LP <= 11: the total is < 32).
+// K given by its four bit masks (K = 16 - (LP - d) <= 15, so the total is at
+// most 16 + d < 32 for d <= 15; the host checks d <= 15 and LP - d <= 16).
 template <int LP>
 __device__ __forceinline__ void slice_count(const uint32_t (&m)[LP], const uint32_t (&k)[4],
                                             uint32_t (&c)[5]) {

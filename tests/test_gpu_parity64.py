@@ -34,7 +34,9 @@ def _gpu():
 
 ACGT = "ACGT"
 WIDE = pms.Launch(wide_words=1)
-FAMILIES64 = [pms.Launch(), pms.Launch(algo=pms.ALGO_BLOCK, block_digits=5),
+FAMILIES64 = [pms.Launch(), pms.Launch(algo=pms.ALGO_SLICE),
+              pms.Launch(algo=pms.ALGO_SLICE, table_global=1),
+              pms.Launch(algo=pms.ALGO_BLOCK, block_digits=5),
               pms.Launch(algo=pms.ALGO_BLOCK, block_digits=6),
               pms.Launch(algo=pms.ALGO_CANDIDATE)]
 
@@ -238,3 +240,28 @@ def test_plan_execute64_with_torch_tensors(orc):
         out32 = torch.zeros(16, dtype=torch.int32, device=dev)
         with pytest.raises(pms.PmsError):
             plan.execute_tensors(seqs, out32, cnt, lo=lo, hi=hi)
+
+
+@pytest.mark.parametrize("l,d", [(17, 5), (19, 7), (21, 8), (23, 9), (25, 10), (28, 12)])
+def test_large_l_slice_family_default(orc, l, d):
+    """l = 17..31 runs the slice family by default (S = 7, LP = l - 7 prefix
+    digits; pms_slice_wide.cu) wherever the prefix counter holds it (d <= 15,
+    LP - d <= 16); with d + S > 15 the sparse mode is off (dense scans only).
+    FM instances at n = 20, t = 600 (the paper's shape at larger (l, d)): the
+    planted consensus is found on a range around it and the set equals the
+    oracle's there and on a random range, every hand-off threshold."""
+    s, rec = fmgen.generate_fm(20, 600, l, d, 2)
+    c = rank_of(rec.consensus)
+    rng = random.Random(l)
+    lo = rng.randrange(0, 4 ** l - 70000)
+    for a, b in ((c - 40000, c + 30001), (lo, lo + 65536)):
+        want = orc.find64(s, l, d, lo=a, hi=b).codes.tolist()
+        for h in (0, 1, 3):
+            got = gpu64(s, l, d, lo=a, hi=b, launch=pms.Launch(handoff=h))
+            assert got.status == 0 and got.codes.tolist() == want, (l, d, a, b, h)
+            assert got.stats.algo == pms.ALGO_SLICE and got.stats.block_digits == 7
+        if a <= c < b:
+            assert c in set(want)
+    # outside the counter's range: the block family
+    r = gpu64(s, 27, 3, lo=c % 4 ** 27, hi=c % 4 ** 27 + 100)  # LP - d = 17
+    assert r.status == 0 and r.stats.algo == pms.ALGO_BLOCK

@@ -38,6 +38,7 @@ def main() -> None:
                     help="time only [lo_frac, hi_frac) of the code space (1.0 = all)")
     ap.add_argument("--hi-frac", type=float, default=1.0)
     ap.add_argument("--block-digits", type=int, default=0)
+    ap.add_argument("--algo", type=int, default=0, help="pms_launch.algo (0: AUTO)")
     ap.add_argument("--oracle-range", type=int, default=200000)
     ap.add_argument("--out", default="")
     args = ap.parse_args()
@@ -50,7 +51,7 @@ def main() -> None:
         c = rank_of(rec.consensus)
         top = 4 ** l
         lo, hi = int(top * args.lo_frac), int(top * args.hi_frac)
-        L = pms.Launch(block_digits=args.block_digits)
+        L = pms.Launch(block_digits=args.block_digits, algo=args.algo)
         pms.find64_ex(s, l, d, lo=c - 4096, hi=c + 4096, launch=L)  # warm-up (plan, module)
         t0 = time.time()
         r = pms.find64_ex(s, l, d, lo=lo, hi=hi, launch=L, max_out=1 << 24)
@@ -63,7 +64,7 @@ def main() -> None:
         row = dict(l=l, d=d, n=args.n, t=args.t, seed=args.seed, lo=lo, hi=hi,
                    candidates=hi - lo, motifs=r.count, search_ms=st.search_ms, wall_s=wall,
                    candidates_per_s=(hi - lo) / (st.search_ms * 1e-3),
-                   block_scans=st.block_scans, block_digits=st.block_digits,
+                   algo=st.algo, block_scans=st.block_scans, block_digits=st.block_digits,
                    grid=st.grid, block=st.block, table_in_smem=st.table_in_smem,
                    consensus_found=(c in set(r.codes.tolist())) if lo <= c < hi else None,
                    oracle_range=[olo, ohi], oracle_range_parity=(got_rng == want),
