@@ -758,9 +758,6 @@ int plan_execute(pms_plan* p, const uint8_t* d_seqs, uint64_t lo, uint64_t hi, v
         // kSparseHandoff candidates together
         if (p->launch.handoff <= 0) sa.handoff = ht ? (p->d >= 5 ? 2 : 1) : p->sparse_handoff;
         if (!ht && sa.handoff > 32) sa.handoff = 32;  // one sparse list entry per lane
-        // the sparse test adds the suffix matches to the prefix counter: K + l
-        // = 16 + d + S must stay below 32 (large l and d: dense scans only)
-        if (!ht && p->d + p->S > 15) sa.handoff = 0;
         int sp_words = 0, sp_blocks = 0;
         if (p->seqpar) {
             sa.spmask = p->d_spmask;

@@ -844,8 +844,9 @@ __device__ __forceinline__ uint32_t slice_sparse_step(const SliceWarp<S, SMEM>& 
     slice_count<LP>(m, w.km, c);
     const uint32_t* sp = a.splanes + (size_t)i * (S * 128) + lane;
     // does the candidate with suffix code x have a window within d here?
-    // (t = c + suffix matches, five planes, no overflow: K + l <= 31;
-    // t >= 16 + S bit-sliced from the low bit up)
+    // (t = c + suffix matches, five planes plus the carry out of bit 4: c <=
+    // 16 + d and the suffix adds <= S, so t < 64; t >= 16 + S bit-sliced from
+    // the low bit up, and any t >= 32 qualifies)
     auto test = [&](const uint32_t (&sm)[S]) -> uint32_t {
         uint32_t s0, s1, s2;
         slice_count3<S>(sm, s0, s1, s2);
@@ -857,12 +858,13 @@ __device__ __forceinline__ uint32_t slice_sparse_step(const SliceWarp<S, SMEM>& 
         k = (c[2] & s2) | (k & (c[2] ^ s2));
         const uint32_t t3 = c[3] ^ k;
         k = c[3] & k;
-        const uint32_t t4 = c[4] | k;
+        const uint32_t t4 = c[4] ^ k;
+        const uint32_t t5 = c[4] & k;  // t >= 32 (only when d + S >= 16)
         const uint32_t t[5] = {t0, t1, t2, t3, t4};
         uint32_t g = kFull;
 #pragma unroll
         for (int b = 0; b < 5; ++b) g = ((kGe >> b) & 1u) ? (t[b] & g) : (t[b] | g);
-        return g & w.vmask;
+        return (g | t5) & w.vmask;
     };
     uint32_t keep = 0;
     // (two candidates per step, their loads overlapped, measured slower:

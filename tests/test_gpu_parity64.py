@@ -246,7 +246,8 @@ def test_plan_execute64_with_torch_tensors(orc):
 def test_large_l_slice_family_default(orc, l, d):
     """l = 17..31 runs the slice family by default (S = 7, LP = l - 7 prefix
     digits; pms_slice_wide.cu) wherever the prefix counter holds it (d <= 15,
-    LP - d <= 16); with d + S > 15 the sparse mode is off (dense scans only).
+    LP - d <= 16); with d + S >= 16 the sparse test's sum can pass 31 (its
+    carry out of bit 4 counts: (23,9), (25,10), (28,12)).
     FM instances at n = 20, t = 600 (the paper's shape at larger (l, d)): the
     planted consensus is found on a range around it and the set equals the
     oracle's there and on a random range, every hand-off threshold."""
