@@ -289,10 +289,19 @@ def run_gpu(args) -> int:
 
     rank, world, local = dist_setup(args.gpus)
     dist = None
+    one_gpu = os.environ.get("BENCH_ONE_GPU") == "1"
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # BENCH_ONE_GPU=1 (tests only): every rank on cuda:0 over gloo, so the
+        # N > 1 code path can be exercised on a one-GPU box; the ranks' kernels
+        # are independent (they never wait on one another), collectives go
+        # through CPU tensors.  Its timings mean nothing.
+        if one_gpu:
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -324,16 +333,17 @@ def run_gpu(args) -> int:
     from paper_1403_1313_b200.shard import shard_range
     lo, hi = shard_range(total, rank, world) if strong else (0, total)
     gcap = 64  # codes gathered per rank per step (a planted instance has ~1)
+    cdev = torch.device("cpu") if one_gpu else dev  # where the collectives' tensors live
     gbuf = torch.zeros(gcap, dtype=torch.int64, device=dev)
-    gcounts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
-    gcodes = [torch.zeros(gcap, dtype=torch.int64, device=dev) for _ in range(world)]
+    gcounts = [torch.zeros(1, dtype=torch.int64, device=cdev) for _ in range(world)]
+    gcodes = [torch.zeros(gcap, dtype=torch.int64, device=cdev) for _ in range(world)]
 
     def step(ev_end=None, pl=step_plan):
         pl.execute_tensors(seqs, out, cnt, lo, hi, stream=stream)
         if strong and dist:  # the exchange step: every rank's count and codes
-            dist.all_gather(gcounts, cnt)
+            dist.all_gather(gcounts, cnt.to(cdev))
             gbuf.copy_(out[:gcap].to(torch.int64))
-            dist.all_gather(gcodes, gbuf)
+            dist.all_gather(gcodes, gbuf.to(cdev))
         if ev_end is not None:  # end of the step's device work, before the host waits
             ev_end.record(stream)
         status, st = pl.wait()
@@ -373,7 +383,7 @@ def run_gpu(args) -> int:
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tmax = sum(step_ms)
     if dist:
-        x = torch.tensor([tmax], device=dev, dtype=torch.float64)
+        x = torch.tensor([tmax], device=cdev, dtype=torch.float64)
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
         tmax = float(x.item())
     nfound = int(cnt.item())
@@ -385,6 +395,14 @@ def run_gpu(args) -> int:
         nfound = sum(counts)
     g = golden(HEADLINE, seed)
     parity = None if g is None else (codes == g["codes"] and nfound == g["count"])
+    # weak scaling: every rank checks its own instance against its golden set
+    # (tests/golden holds (15,4) seeds 1-8); 1 / 0 / -1 = equal / differs / no golden
+    parity_ranks = None
+    if dist and not strong:
+        pr = torch.zeros(world, dtype=torch.int64, device=cdev)
+        pr[rank] = -1 if parity is None else int(parity)
+        dist.all_reduce(pr)
+        parity_ranks = [None if v < 0 else bool(v) for v in pr.cpu().tolist()]
     search_avg = float(np.mean(search_ms))
     cs = clk.summary()
     sms = pms.device_info()["sms"]
@@ -401,7 +419,7 @@ def run_gpu(args) -> int:
             e2e_ms.append(1e3 * dt)
     e2e_tot = float(sum(e2e_ms))
     if dist:
-        x = torch.tensor([e2e_tot], device=dev, dtype=torch.float64)
+        x = torch.tensor([e2e_tot], device=cdev, dtype=torch.float64)
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
         e2e_tot = float(x.item())
 
@@ -486,6 +504,7 @@ def run_gpu(args) -> int:
                          "steps again with the pre-pass/search event, same input, L2 flushed",
         "block_scans_per_launch": int(last.block_scans),
         "motifs": nfound, "parity_vs_golden": parity,
+        **({"parity_vs_golden_ranks": parity_ranks} if parity_ranks is not None else {}),
         "roofline": roof,
         "candidate_kernel": cand,
         "cpu_baseline": cpu,
@@ -496,7 +515,8 @@ def run_gpu(args) -> int:
                 # small sets), + the codes again when the set is larger than that
                 "d2h_bytes_per_step": 128 + 4 * min(cap, 1024) + (4 * nfound if nfound > 1024 else 0),
                 "path": "pms_find_ex from host buffers (pooled context, H2D, kernels, D2H, sort)"},
-        "gpu_launches": 2 * args.steps,
+        # pre-pass + search per step per rank (the untimed L2 flush is torch's fill)
+        "gpu_launches": 2 * args.steps * world,
         "clocks": cs,
     }
     print(json.dumps(line), flush=True)

@@ -7,7 +7,7 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 rm -rf /tmp/base && mkdir -p /tmp/base
 git -C "$ROOT" archive "$REV" paper_1403_1313_b200 include | tar -x -C /tmp/base
 cd /tmp/base
-for f in pms pms64 pms_slice pms_slice_ht pms_roof; do
+for f in pms pms64 pms_slice pms_slice_ht pms_slice_wide pms_roof; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -O3 \
        -I include -I paper_1403_1313_b200/csrc -c paper_1403_1313_b200/csrc/$f.cu -o /tmp/base/$f.o &
 done

@@ -12,9 +12,23 @@ ap = argparse.ArgumentParser()
 ap.add_argument("csv")
 ap.add_argument("--units", type=float, required=True)
 ap.add_argument("--top", type=int, default=25)
+ap.add_argument("--wavefronts", action="store_true",
+                help="instead: the instructions with most shared-memory wavefronts per unit")
 args = ap.parse_args()
 rows = list(csv.reader(open(args.csv)))
 hdr = rows[1]
+if args.wavefronts:
+    iw, ii, ie, isr = (hdr.index("L1 Wavefronts Shared"), hdr.index("L1 Wavefronts Shared Ideal"),
+                       hdr.index("Instructions Executed"), hdr.index("Source"))
+    out = [(n, r[isr].strip(), int(r[ie] or 0), int(r[iw] or 0), int(r[ii] or 0))
+           for n, r in enumerate(rows[2:]) if len(r) > iw and int(r[iw] or 0)]
+    tot, ideal = sum(o[3] for o in out), sum(o[4] for o in out)
+    print(f"shared-memory wavefronts {tot} = {tot / args.units:.1f} per unit "
+          f"(ideal {ideal / args.units:.1f}: the rest are bank conflicts / same-address atomics)")
+    for n, src, ex, w, idl in sorted(out, key=lambda o: -o[3])[:args.top]:
+        print(f"sass {n:5d} {src[:52]:52s} exec/unit {ex / args.units:6.2f}  wavefronts/unit "
+              f"{w / args.units:6.2f}  per instruction {w / max(ex, 1):5.2f}")
+    raise SystemExit(0)
 ix, isrc, iex, ismp = (hdr.index("Address"), hdr.index("Source"), hdr.index("Instructions Executed"),
                       hdr.index("Warp Stall Sampling (All Samples)"))
 ins = [(i, r[isrc].strip(), int(r[iex] or 0), int(r[ismp] or 0)) for i, r in enumerate(rows[2:]) if len(r) > iex]

@@ -34,6 +34,15 @@ KEYS = [
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed.avg.per_cycle_active", "smsp__inst_executed.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    # the L1 data pipe (shared-memory wavefronts: one per cycle per SM)
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+    "smsp__inst_executed_op_shared_atom.sum",
+    "memory_l1_wavefronts_shared", "memory_l1_wavefronts_shared_ideal",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
     "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
@@ -88,7 +97,11 @@ def to_json(rep: str, scans: int, out: str, kernel_note: str, config: str = "") 
            "xu_pipe_pct": num("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
            "kernel_us": num("gpu__time_duration.sum") / (1e3 if "nsecond" in units[hdr.index(
                "gpu__time_duration.sum")] else 1.0),
-           "shared_bank_conflicts": num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")}
+           "shared_bank_conflicts": num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+           "l1_data_pipe_pct": num("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+           "shared_wavefronts_per_scan": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum") / scans,
+           "shared_atom_wavefronts_per_scan":
+               num("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum") / scans}
     with open(out, "w") as f:
         json.dump(doc, f, indent=1)
         f.write("\n")

@@ -127,3 +127,38 @@ def test_sharded_cuda_path_against_golden(orc, world):
         # range additivity: the shard union over a window around the plant
         near = orc.find64(s17, 17, 4, lo=max(0, cons - 50000), hi=cons + 50000).codes.tolist()
         assert [c for c in got[2] if cons - 50000 <= c < cons + 50000] == near
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_two_ranks_one_gpu(scaling):
+    """`bench.py --gpus 2` launched as the driver launches it (torch.distributed.run,
+    one process per rank), with BENCH_ONE_GPU=1: both ranks on cuda:0 over gloo
+    (this pool has one GPU; the ranks' kernels never wait on one another).
+    Checks the N > 1 line: whole-job value over both ranks, the seeds, and
+    parity -- weak: every rank's own instance against its golden set; strong:
+    the gathered union of the two range shards."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BENCH_ONE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "5", "--warmup", "3",
+           "--e2e-steps", "2", "--scaling", scaling]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["steps"] == 5 and line["scaling"] == scaling
+    assert line["parity_vs_golden"] is True
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    if scaling == "weak":
+        assert line["config"]["seeds"] == [1, 2]
+        assert line["parity_vs_golden_ranks"] == [True, True]
+        # two instances per step: the whole-job value counts both
+        assert abs(line["value"] - 2 * 4 ** 15 / (line["ms_per_step"] * 1e-3)) < 1e-3 * line["value"]
+    else:
+        assert line["config"]["seeds"] == [1]
