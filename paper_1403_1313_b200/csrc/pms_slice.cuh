@@ -52,7 +52,7 @@ namespace pms {
 struct SliceArgs {
     const uint32_t* planes;   // [n][LP][4][32] match planes (global)
     const uint32_t* splanes;  // [n][S][4][32] match planes of the suffix positions (sparse mode)
-    const uint16_t* slots;    // [n][Wp] r = 0 slot of each window (global)
+    const uint16_t* slots;    // [n][Wp] r = 0 slot of each window (global; row order: slot_idx)
     const uint32_t* words;    // [n][Wp] packed Bp32 windows (hand-off checks, global)
     const uint32_t* ball;     // slice ball table (kSTWords words, global)
     int n, W, Wp, NWl;        // Wp = 32 * NWl
@@ -121,6 +121,16 @@ constexpr int kSliceMaxLP = 24;              // l <= 31 (S = 7); LP - d <= 16, d
 #endif
 #ifndef PMS_SLICE_R1_DIRECT
 #define PMS_SLICE_R1_DIRECT 0  // r = 1 hits resolved per lane (NU reds each); 0: queued
+#endif
+#ifndef PMS_SLICE_CHECK_VOTE
+#define PMS_SLICE_CHECK_VOTE 1  // tables hand-off check: hit classes r >= 2, 1, 0 with a vote per step
+#endif
+#ifndef PMS_SLICE_SLOTS_QMAJOR
+// slot rows stored bit-major -- window (lane L, bit q) at q * 32 + L -- so the
+// lanes of a hit loop, each at its own q, read 2-byte slots that share banks
+// only within a lane pair (window-major rows: L * NWl + q, birthday conflicts,
+// ~2 wavefronts per LDS.U16 in the ncu source page)
+#define PMS_SLICE_SLOTS_QMAJOR 1
 #endif
 constexpr uint32_t kSpDead = 0x80000000u;     // spcnt flag: the block's AND is empty
 constexpr uint32_t kPoison16 = 0xFFFFu;      // debug builds: consumed / unwritten queue entry
@@ -234,7 +244,12 @@ __global__ void __launch_bounds__(kSlicePackThreads) pms_pack_slice(
         const uint32_t kw = ((eH >> 5) << X) | (eL >> 5);
         // slot = byte offset of the candidate's word in the warp's block
         // (word = k * 32 + lane, word-major; < 2 KB at S <= 7) | bit << 11
-        slots[(long long)i * Wp + k] =
+#if PMS_SLICE_SLOTS_QMAJOR
+        const int kslot = (k % NWl) * 32 + k / NWl;
+#else
+        const int kslot = k;
+#endif
+        slots[(long long)i * Wp + kslot] =
             (uint16_t)(k < W ? (((kw * 32u + (eH & 31u)) * 4u) | ((eL & 31u) << 11)) : 0u);
     } else if (item < Wp + l * 128) {
         // positions j < LP: the staged prefix planes; j >= LP: the suffix
@@ -339,6 +354,16 @@ __device__ __forceinline__ uint32_t atom_add(uint32_t a, uint32_t v) {
     uint32_t r;
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
     return r;
+}
+
+// index of window (lane, bit q) in a sequence's slot row
+__device__ __forceinline__ uint32_t slot_idx(uint32_t lane, uint32_t q, int NWl) {
+#if PMS_SLICE_SLOTS_QMAJOR
+    (void)NWl;
+    return q * 32u + lane;
+#else
+    return lane * (uint32_t)NWl + q;
+#endif
 }
 
 // r = d - p of the hit at bit q (the low four counter planes)
@@ -536,12 +561,12 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
     constexpr int X = C::X, NU = C::NU;
     const uint32_t lane = w.lane;
     // slot row of this lane's windows in sequence i
-    const uint32_t srow = (uint32_t)(i * w.Wp) + lane * (uint32_t)w.NWl;
+    const uint32_t srow = (uint32_t)(i * w.Wp) + slot_idx(lane, 0u, w.NWl);
     const uint32_t srow_s = w.slots_s + 2u * srow;
     auto slot_of = [&](int q) -> uint32_t {
-        PMS_CHECK((int)lane * w.NWl + q < w.Wp);
-        if constexpr (SMEM) return lds16(srow_s + 2u * (uint32_t)q);
-        else return __ldg(w.gslots + srow + (uint32_t)q);
+        PMS_CHECK((int)lane * w.NWl + q < w.Wp && q < w.NWl);
+        if constexpr (SMEM) return lds16(srow_s + 2u * slot_idx(0u, (uint32_t)q, w.NWl));
+        else return __ldg(w.gslots + srow + slot_idx(0u, (uint32_t)q, w.NWl));
     };
 #ifdef PMS_DEBUG_CHECKS
     // protocol check: the candidate words and the queue counter are clear at
@@ -781,18 +806,46 @@ __device__ __forceinline__ bool slice_check_one(const SliceWarp<S, SMEM>& w, con
         uint32_t c[5], r0m, r1m, r2m;
         slice_pass1<S, LP, SMEM>(w, po, i, c, r0m, r1m, r2m);
         ++scanned;
-        const uint32_t srow = (uint32_t)(i * w.Wp) + w.lane * (uint32_t)w.NWl;
+        const uint32_t srow = (uint32_t)(i * w.Wp) + slot_idx(w.lane, 0u, w.NWl);
+#if PMS_SLICE_CHECK_VOTE
+        // The hit classes in the order an occurrence is most likely found --
+        // r >= 2, r = 1, r = 0: a planted window at distance d has on average
+        // d * LP / l of its mismatches in the prefix, while a chance prefix hit
+        // is mostly at prefix distance d (r = 0) -- with warp-uniform trip
+        // counts and a vote per iteration, so the warp stops at the first
+        // match any lane finds instead of waiting for the lane with most hits
+        // (this check is a lone warp's chain, the tail of the latency
+        // instances; the result -- some window within d -- is the same)
+        auto any_match = [&](uint32_t hv) -> bool {
+            const uint32_t trips = __reduce_max_sync(kFull, (uint32_t)__popc(hv));
+            for (uint32_t it = 0; it < trips; ++it) {
+                bool f = false;
+                if (hv) {
+                    const int q = msb(hv);
+                    hv ^= 1u << q;
+                    PMS_CHECK((int)w.lane * w.NWl + q < w.Wp);
+                    const uint32_t sl = SMEM ? lds16(w.slots_s + 2u * (srow + slot_idx(0u, (uint32_t)q, w.NWl)))
+                                             : (uint32_t)__ldg(w.gslots + srow + slot_idx(0u, (uint32_t)q, w.NWl));
+                    f = slice_sfx_dist<S>(sl ^ sx) <= slice_r(c, q);
+                }
+                if (__any_sync(kFull, f)) return true;
+            }
+            return false;
+        };
+        if (!(any_match(r2m) || any_match(r1m) || any_match(r0m))) return false;
+#else
         bool f = false;
         uint32_t hv = r0m | r1m | r2m;
         while (hv && !f) {
             const int q = msb(hv);
             hv ^= 1u << q;
             PMS_CHECK((int)w.lane * w.NWl + q < w.Wp);
-            const uint32_t sl = SMEM ? lds16(w.slots_s + 2u * (srow + (uint32_t)q))
-                                     : (uint32_t)__ldg(w.gslots + srow + (uint32_t)q);
+            const uint32_t sl = SMEM ? lds16(w.slots_s + 2u * (srow + slot_idx(0u, (uint32_t)q, w.NWl)))
+                                     : (uint32_t)__ldg(w.gslots + srow + slot_idx(0u, (uint32_t)q, w.NWl));
             f = slice_sfx_dist<S>(sl ^ sx) <= slice_r(c, q);
         }
         if (!__any_sync(kFull, f)) return false;
+#endif
     }
     return true;
 }
