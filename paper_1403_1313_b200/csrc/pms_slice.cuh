@@ -132,6 +132,9 @@ constexpr int kSliceMaxLP = 24;              // l <= 31 (S = 7); LP - d <= 16, d
 // ~2 wavefronts per LDS.U16 in the ncu source page)
 #define PMS_SLICE_SLOTS_QMAJOR 1
 #endif
+#ifndef PMS_SLICE_PIN_WQ
+#define PMS_SLICE_PIN_WQ 1  // the warp's queue-block address pinned in a register
+#endif
 constexpr uint32_t kSpDead = 0x80000000u;     // spcnt flag: the block's AND is empty
 constexpr uint32_t kPoison16 = 0xFFFFu;      // debug builds: consumed / unwritten queue entry
 constexpr uint32_t kPoison32 = 0xFFFFFFFFu;  // (no real entry: slots < 2^14, r < 16)
@@ -161,9 +164,17 @@ struct SliceCfg {
     static constexpr uint32_t kAccAlign = 32u * KW * 4u;  // one warp's word block
     static constexpr uint32_t kAccOff = kSTWords * 4u;     // (+ up to kAccAlign - 1 at run time)
     static constexpr uint32_t kAccBytes = NWARP * 32u * KW * 4u + kAccAlign;
-    static constexpr uint32_t kQ01Off = kAccOff + kAccBytes;
-    static constexpr uint32_t kQ2Off = kQ01Off + NWARP * (kCap0 + kCap1) * 2u;
-    static constexpr uint32_t kWorkBytes = kQ2Off + NWARP * kCap2 * 4u;  // = planes offset
+    // one queue block per warp -- [r = 0 queue][r = 1 queue][r >= 2 queue]
+    // [claim counter, padded to 16 B] -- so every queue address is one per-warp
+    // base plus a compile-time offset (separate arrays had the compiler
+    // re-derive four bases from %tid and the shared window every scan: five
+    // S2R and ~20 instructions per scan in the SASS)
+    static constexpr uint32_t kQ1Rel = kCap0 * 2u;
+    static constexpr uint32_t kQ2Rel = kQ1Rel + kCap1 * 2u;
+    static constexpr uint32_t kQcRel = kQ2Rel + kCap2 * 4u;
+    static constexpr uint32_t kQStride = kQcRel + 16u;
+    static constexpr uint32_t kQOff = kAccOff + kAccBytes;
+    static constexpr uint32_t kWorkBytes = kQOff + NWARP * kQStride;  // = planes offset
     static_assert(kWorkBytes % 128u == 0, "TMA destinations");
 };
 
@@ -429,7 +440,11 @@ __device__ __forceinline__ void slice_bcast(uint32_t e, uint32_t lane4, uint32_t
 template <int S, bool SMEM>
 struct SliceWarp {
     using C = SliceCfg<S>;
-    uint32_t lane, acc_s, q0_s, q1_s, q2_s, qc_s, T_s, R1_s, slots_s;
+    uint32_t lane, acc_s, wq_s, T_s, R1_s, slots_s;  // wq_s: the warp's queue block
+    __device__ __forceinline__ uint32_t q0_s() const { return wq_s; }
+    __device__ __forceinline__ uint32_t q1_s() const { return wq_s + C::kQ1Rel; }
+    __device__ __forceinline__ uint32_t q2_s() const { return wq_s + C::kQ2Rel; }
+    __device__ __forceinline__ uint32_t qc_s() const { return wq_s + C::kQcRel; }
     uint32_t lane4, acc_lane_s;  // 4 * lane; acc_s + 4 * lane (the lane's word 0)
     uint32_t planes_s;           // shared-window address of the staged planes (SMEM)
     const uint32_t* planes;  // shared (SMEM) or global
@@ -445,7 +460,7 @@ struct SliceWarp {
 // (SMEM) the planes and slots, completion on an mbarrier.
 template <int S, bool SMEM>
 __device__ __forceinline__ SliceWarp<S, SMEM> slice_setup(const SliceArgs& a, uint32_t* sdyn,
-                                                         uint64_t* bar, uint32_t* qcnts) {
+                                                         uint64_t* bar) {
     using C = SliceCfg<S>;
     constexpr int KW = C::KW;
     SliceWarp<S, SMEM> w;
@@ -458,20 +473,20 @@ __device__ __forceinline__ SliceWarp<S, SMEM> slice_setup(const SliceArgs& a, ui
     w.acc_s = acc0_s + wid * C::kAccAlign;
     w.lane4 = w.lane * 4u;
     w.acc_lane_s = w.acc_s + w.lane4;
-    w.q0_s = dyn_s + C::kQ01Off + wid * ((C::kCap0 + C::kCap1) * 2u);
-    w.q1_s = w.q0_s + 2u * C::kCap0;
-    w.q2_s = dyn_s + C::kQ2Off + wid * (C::kCap2 * 4u);
-    w.qc_s = smem_u32(&qcnts[wid]);
+    w.wq_s = dyn_s + C::kQOff + wid * C::kQStride;
+#if PMS_SLICE_PIN_WQ
+    asm volatile("" : "+r"(w.wq_s));  // opaque: held in a register, not re-derived per scan
+#endif
     PMS_CHECK((w.acc_s & (32u * KW * 4u - 1u)) == 0u);
 #pragma unroll
     for (int k = 0; k < KW; ++k) sts32(w.acc_s + (k * 32u + w.lane) * 4u, 0u);
-    if (w.lane == 0) sts32(w.qc_s, 0u);
+    if (w.lane == 0) sts32(w.qc_s(), 0u);
 #ifdef PMS_DEBUG_CHECKS
     // protocol check: every queue entry starts poisoned and is
     // poisoned again once consumed, so a round that reads an entry nobody
     // wrote this scan (a missed __syncwarp, a bad claim) is counted
-    for (int q = (int)w.lane; q < C::kCap0 + C::kCap1; q += 32) sts16(w.q0_s + 2u * q, kPoison16);
-    for (int q = (int)w.lane; q < C::kCap2; q += 32) sts32(w.q2_s + 4u * q, kPoison32);
+    for (int q = (int)w.lane; q < C::kCap0 + C::kCap1; q += 32) sts16(w.q0_s() + 2u * q, kPoison16);
+    for (int q = (int)w.lane; q < C::kCap2; q += 32) sts32(w.q2_s() + 4u * q, kPoison32);
 #endif
     uint32_t* splanes = sdyn + C::kWorkBytes / 4u;
     uint16_t* sslots = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(splanes) + a.plane_bytes);
@@ -493,11 +508,23 @@ __device__ __forceinline__ SliceWarp<S, SMEM> slice_setup(const SliceArgs& a, ui
     }
     mbar_wait(bar, 0);
     w.planes = SMEM ? splanes : a.planes;
-    w.planes_s = smem_u32(splanes);
     w.gslots = a.slots;
+#if PMS_SLICE_PIN_WQ
+    // the table addresses as one opaque base plus offsets: the compiler
+    // otherwise re-derives each from the shared window (S2R SR_CgaCtaId + MOV
+    // + VIADD + LEA) wherever it is used, five times per scan in the SASS
+    uint32_t base_s = dyn_s;
+    asm volatile("" : "+r"(base_s));
+    w.T_s = base_s;
+    w.R1_s = base_s + 4u * kSR1Off;
+    w.planes_s = base_s + C::kWorkBytes;
+    w.slots_s = base_s + C::kWorkBytes + a.plane_bytes;
+#else
+    w.planes_s = smem_u32(splanes);
     w.T_s = dyn_s;
     w.R1_s = dyn_s + 4u * kSR1Off;
     w.slots_s = smem_u32(sslots);
+#endif
     for (int b = 0; b < 4; ++b) w.km[b] = a.kmask[b];
     const int nvalid = min(a.NWl, max(0, a.W - (int)w.lane * a.NWl));
     w.vmask = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
@@ -573,7 +600,7 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
     // the start of every scan (cleared by the previous scan's end)
 #pragma unroll
     for (int k = 0; k < C::KW; ++k) PMS_CHECK(lds32(w.acc_s + (k * 32u + lane) * 4u) == 0u);
-    if (lane == 0) PMS_CHECK(lds32(w.qc_s) == 0u);
+    if (lane == 0) PMS_CHECK(lds32(w.qc_s()) == 0u);
 #endif
 #if PMS_SLICE_R0_DIRECT
     // r = 0 hits (~80 %) resolved by the finding lane, no queue: one slot load
@@ -624,10 +651,10 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
         // 5-step shuffle prefix sum instead measured +16 % at (15,4)), then
         // resolve them full-width
         if (n012) {
-            const uint32_t pos = atom_add(w.qc_s, n012);
-            uint32_t a0 = w.q0_s + 2u * (pos & 1023u);
-            uint32_t a1 = w.q1_s + 2u * ((pos >> 10) & 1023u);
-            uint32_t a2 = w.q2_s + 4u * (pos >> 20);
+            const uint32_t pos = atom_add(w.qc_s(), n012);
+            uint32_t a0 = w.q0_s() + 2u * (pos & 1023u);
+            uint32_t a1 = w.q1_s() + 2u * ((pos >> 10) & 1023u);
+            uint32_t a2 = w.q2_s() + 4u * (pos >> 20);
             while (r0m) {
                 const int q = msb(r0m);
                 r0m ^= 1u << q;
@@ -648,10 +675,10 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
             }
         }
         __syncwarp();
-        if (lane == 0) sts32(w.qc_s, 0u);  // claims are done; next use after __syncwarp
+        if (lane == 0) sts32(w.qc_s(), 0u);  // claims are done; next use after __syncwarp
         // loop-invariant shared-window addresses, pinned in registers: under the
         // 64-register cap the compiler otherwise re-derives them every round
-        uint32_t acc = w.acc_s, qa0 = w.q0_s + 2u * lane;
+        uint32_t acc = w.acc_s, qa0 = w.q0_s() + 2u * lane;
         asm volatile("" : "+r"(acc), "+r"(qa0));
         // round loops with warp-uniform trip counts and predicated bodies: a
         // lane-dependent trip count let the warp run on diverged into the
@@ -672,7 +699,7 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
         // words of a hit -- same lane, same bank -- in one ~7-wavefront red),
         // and no per-lane update decode
         if (t1) {
-            uint32_t qh = w.q1_s + 2u * lane;
+            uint32_t qh = w.q1_s() + 2u * lane;
             asm volatile("" : "+r"(qh));
 #pragma unroll 1
             for (uint32_t b1 = 0; b1 < t1; b1 += 32u, qh += 64u) {
@@ -694,23 +721,23 @@ __device__ __forceinline__ void slice_pass2(const SliceWarp<S, SMEM>& w, int i,
         if (w.rclamp) {
 #pragma unroll 1
             for (uint32_t b2 = 0; b2 < t2; ++b2) {
-                const uint32_t e = lds32(w.q2_s + 4u * b2);  // same address: broadcast
+                const uint32_t e = lds32(w.q2_s() + 4u * b2);  // same address: broadcast
                 PMS_CHECK(e != kPoison32);
                 slice_bcast<X, true>(e, w.lane4, w.T_s, w.acc_lane_s, common);
             }
         } else {
 #pragma unroll 1
             for (uint32_t b2 = 0; b2 < t2; ++b2) {
-                const uint32_t e = lds32(w.q2_s + 4u * b2);
+                const uint32_t e = lds32(w.q2_s() + 4u * b2);
                 PMS_CHECK(e != kPoison32 && (e >> 16) <= 6u);
                 slice_bcast<X, false>(e, w.lane4, w.T_s, w.acc_lane_s, common);
             }
         }
 #ifdef PMS_DEBUG_CHECKS
         __syncwarp();  // every lane has read its entries: poison them again
-        for (uint32_t q = lane; q < t0; q += 32u) sts16(w.q0_s + 2u * q, kPoison16);
-        for (uint32_t q = lane; q < t1; q += 32u) sts16(w.q1_s + 2u * q, kPoison16);
-        for (uint32_t q = lane; q < t2; q += 32u) sts32(w.q2_s + 4u * q, kPoison32);
+        for (uint32_t q = lane; q < t0; q += 32u) sts16(w.q0_s() + 2u * q, kPoison16);
+        for (uint32_t q = lane; q < t1; q += 32u) sts16(w.q1_s() + 2u * q, kPoison16);
+        for (uint32_t q = lane; q < t2; q += 32u) sts32(w.q2_s() + 4u * q, kPoison32);
 #endif
     } else {
         // dense hits (a queue would overflow): per-lane resolution
@@ -995,7 +1022,8 @@ template <int S, int LP, bool SMEM, bool HT = false>
 __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs a) {
     using B = BlkTraits<S>;
     using C = SliceCfg<S>;
-    constexpr int KW = C::KW, NWARP = C::NWARP;
+    constexpr int KW = C::KW;
+    [[maybe_unused]] constexpr int NWARP = C::NWARP;  // (trace builds)
     static_assert(LP >= 1 && LP <= kSliceMaxLP, "prefix length");
     // [ball table][candidate words][queues][planes][slots] (SliceCfg); each
     // warp's word block is aligned to its size, so a word index XOR is an
@@ -1004,14 +1032,13 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice(SliceArgs
     // compiler would fold it.
     extern __shared__ __align__(128) uint32_t sdyn[];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ uint32_t qcnts[NWARP];
 #ifdef PMS_TRACE
     const unsigned long long tr_enter = gtimer();
     unsigned long long tr_blocks = 0, tr_hand = 0, tr_maxs = 0, tr_maxt = 0;
 #endif
     pdl_wait();
     if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
-    const SliceWarp<S, SMEM> w = slice_setup<S, SMEM>(a, sdyn, &bar, qcnts);
+    const SliceWarp<S, SMEM> w = slice_setup<S, SMEM>(a, sdyn, &bar);
     const uint32_t lane = w.lane;
     unsigned long long scanned = 0, bscans = 0;
 #ifdef PMS_TRACE
@@ -1154,17 +1181,17 @@ template <int S, int LP>
 __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_search_slice_sp(SliceArgs a) {
     using B = BlkTraits<S>;
     using C = SliceCfg<S>;
-    constexpr int KW = C::KW, NWARP = C::NWARP;
+    constexpr int KW = C::KW;
+    [[maybe_unused]] constexpr int NWARP = C::NWARP;  // (trace builds)
     extern __shared__ __align__(128) uint32_t sdyn[];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ uint32_t qcnts[NWARP];
 #ifdef PMS_TRACE
     const unsigned long long tr_enter = gtimer();
     unsigned long long tr_units = 0;
 #endif
     pdl_wait();
     if (*(volatile unsigned int*)&a.st->bad == a.epoch) return;
-    const SliceWarp<S, true> w = slice_setup<S, true>(a, sdyn, &bar, qcnts);
+    const SliceWarp<S, true> w = slice_setup<S, true>(a, sdyn, &bar);
     const uint32_t lane = w.lane;
     const unsigned long long nunits = a.sp_blocks * (unsigned long long)a.n;
     unsigned long long bscans = 0;
@@ -1273,8 +1300,7 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
     constexpr int KW = C::KW, NWARP = C::NWARP;
     extern __shared__ __align__(128) uint32_t sdyn[];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ uint32_t qcnts[NWARP];
-    const SliceWarp<S, SMEM> w = slice_setup<S, SMEM>(a, sdyn, &bar, qcnts);
+    const SliceWarp<S, SMEM> w = slice_setup<S, SMEM>(a, sdyn, &bar);
     const unsigned long long warps = (unsigned long long)gridDim.x * NWARP;
     const unsigned long long g = (unsigned long long)blockIdx.x * NWARP + (threadIdx.x >> 5);
     uint32_t acc = 0;
