@@ -159,8 +159,8 @@ struct SliceCfg {
     static constexpr int kCap1 = S >= 7 ? 96 : 128;
     static constexpr int kCap2 = S >= 7 ? 32 : 64;
     // dynamic shared memory in front of the staged tables: [ball table]
-    // [per-warp candidate words][r = 0 / 1 queues][r >= 2 queues]; the word
-    // blocks start at a multiple of their size (30 KB = 15 x 2 KB)
+    // [per-warp candidate words][per-warp queue blocks]; the word blocks
+    // start at a multiple of their size (30 KB = 15 x 2 KB)
     static constexpr uint32_t kAccAlign = 32u * KW * 4u;  // one warp's word block
     static constexpr uint32_t kAccOff = kSTWords * 4u;     // (+ up to kAccAlign - 1 at run time)
     static constexpr uint32_t kAccBytes = NWARP * 32u * KW * 4u + kAccAlign;
