@@ -1305,6 +1305,7 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
     const unsigned long long g = (unsigned long long)blockIdx.x * NWARP + (threadIdx.x >> 5);
     uint32_t acc = 0;
     unsigned long long blk = g % nblocks;
+    const unsigned long long bstep = warps % nblocks;
     int i = 0;
     const uint32_t A = (uint32_t)min(max(a.handoff, 1), 32);
     // a fixed pseudo-random candidate list per warp (modes 2, 3)
@@ -1316,15 +1317,19 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
     // fall on the same scans (in the search they come whenever a block's
     // survivors drop below the threshold)
     uint32_t credit = (uint32_t)(g * 40503u) & 0xFFFFu;
+    // the block's plane offsets change with the block, not with the scan (as in
+    // the search kernel: computed once per block)
+    uint32_t po[LP];
+    slice_offsets<S, LP>(blk << (2 * S), w.lane, po);
 #pragma unroll 1
     for (int k = 0; k < scans; ++k) {
-        uint32_t po[LP];
-        slice_offsets<S, LP>(blk << (2 * S), w.lane, po);
+        if (i == 0 && k) slice_offsets<S, LP>(blk << (2 * S), w.lane, po);
         if constexpr (MODE == 2) {
             acc ^= slice_sparse_step<S, LP, SMEM>(w, a, po, i, w.acc_s, A);
             if (++i == depth) {
                 i = 0;
-                blk = (blk + warps) % nblocks;
+                blk += bstep;  // = (blk + warps) % nblocks without a 64-bit division per block
+                if (blk >= nblocks) blk -= nblocks;
             }
             continue;
         }
@@ -1334,6 +1339,9 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
             acc ^= r0m ^ (r1m << 1) ^ (r2m << 2);
         } else {
             slice_pass2<S, SMEM>(w, i, c, r0m, r1m, r2m, common);
+            // (alive reset every scan: keeping it live across a block's scans,
+            // as the search must, measured 3.7 % slower -- register pressure --
+            // so this is the higher, more conservative ceiling)
             uint32_t alive[KW];
 #pragma unroll
             for (int q = 0; q < KW; ++q) alive[q] = kFull;
@@ -1358,7 +1366,8 @@ __global__ void __launch_bounds__(SliceCfg<S>::NT, 1) pms_roofline_slice(SliceAr
         }
         if (++i == depth) {
             i = 0;
-            blk = (blk + warps) % nblocks;
+            blk += bstep;  // = (blk + warps) % nblocks without a 64-bit division per block
+            if (blk >= nblocks) blk -= nblocks;
         }
     }
     if (acc == 0x9E3779B9u) sink[0] = acc;  // keeps the work live
