@@ -69,6 +69,11 @@ def main() -> int:
                 fails += 1
                 print(f"FAIL32 n={n} t={t} l={l} d={d} seed={seed} lo={lo} hi={hi}", flush=True)
     print(f"stress: {runs} runs, {fails} failures")
+    if os.environ.get("PMS_DEBUG_LIB") == "1":
+        # the bounds / protocol-checked library: failed device checks over the whole run
+        v = pms.debug_violations()
+        print(f"stress: {v} debug-check violations")
+        fails += int(v != 0)
     return 1 if fails else 0
 
 
